@@ -1,0 +1,207 @@
+/*
+ * uc_b200.h — C ABI of the B200-native hot path of the Tusas/undercool JFNK
+ * phase-field solver (arXiv:2006.16764).
+ *
+ * All vector arguments are DEVICE pointers to fp64 arrays in the reference's
+ * block-by-field layout (all nodes of field 0, then all nodes of field 1;
+ * nodes lexicographic with x fastest — undercool/assembly.py:48-54,
+ * undercool/mesh.py:209-228).  Every entry point is asynchronous on the
+ * context's CUDA stream unless it says it synchronises.  Return codes:
+ *
+ *   UC_OK (0)            success
+ *   UC_ERR_NONFINITE (1) a non-finite value was detected (see uc_status)
+ *   UC_ERR_ARG (2)       bad argument (message in uc_last_error())
+ *   UC_ERR_CUDA (3)      CUDA / NCCL failure
+ *   UC_ERR_UNSUPPORTED (4)
+ *
+ * The reference is pure Python (numpy/scipy/numba); it has no FFI of its own.
+ * Each entry point below names the reference function it replaces; the
+ * ctypes binding a maintainer of the reference would add is in
+ * INTEGRATION.md.  No torch types appear in this interface.
+ */
+#ifndef UC_B200_H
+#define UC_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define UC_OK 0
+#define UC_ERR_NONFINITE 1
+#define UC_ERR_ARG 2
+#define UC_ERR_CUDA 3
+#define UC_ERR_UNSUPPORTED 4
+
+#define UC_MODEL_FREE_GROWTH 1
+#define UC_MODEL_ALLOY 2
+
+#define UC_PART_NEW 0
+#define UC_PART_OLD 1
+
+#define UC_PC_IDENTITY 0
+#define UC_PC_JACOBI 1
+#define UC_PC_SGS 2
+#define UC_PC_VCYCLE 3
+
+typedef struct uc_ctx uc_ctx;
+
+/* Structured Q1 mesh (undercool/mesh.py:179-256 build_mesh).  spacing[a] must
+ * equal extents[a]/counts[a] as the reference computes it.  A rank owns node
+ * planes [slab_lo, slab_hi) along the slowest axis (y in 2D, z in 3D); a
+ * single GPU owns [0, counts[dim-1]+1). */
+typedef struct uc_mesh_desc {
+  int32_t dim;
+  int32_t order;
+  int64_t counts[3];
+  double spacing[3];
+  int64_t slab_lo;
+  int64_t slab_hi;
+} uc_mesh_desc;
+
+/* Physics constants, derived on the host exactly as the reference's kernel
+ * wrappers derive them (free_growth.py:163-206, alloy.py:225-269). */
+typedef struct uc_model_params {
+  int32_t model;          /* UC_MODEL_* */
+  int32_t normalized;     /* alloy: antitrapping_normalized */
+  double eps;             /* anisotropy_strength */
+  double reg;             /* aniso_reg_grad**4 */
+  double aniso_reg_grad;  /* blend scale used by fourfold() in the preconditioner */
+  /* free growth */
+  double bg;              /* kinetic_coeff * mobility */
+  double beta;            /* kinetic_coeff */
+  double alpha;           /* thermal_diffusivity */
+  double latent;          /* latent_ratio */
+  double hcell;           /* mesh_scale */
+  double tmelt;           /* melt_temperature */
+  /* alloy */
+  double at_reg2;         /* antitrap_reg_grad**2 */
+  double kpart;           /* partition */
+  double coupling;
+  double dcoef;           /* diffusivity */
+  double g4_coef;         /* frame_coefficient */
+  double pull_velocity;
+} uc_model_params;
+
+/* ThetaScheme (undercool/stepping.py:12-37). */
+typedef struct uc_scheme {
+  double theta;
+  double dt;
+  int64_t step;
+} uc_scheme;
+
+/* PrecondConfig (undercool/precond.py:54-71); ordering is always multicolor. */
+typedef struct uc_precond_cfg {
+  int32_t kind;           /* UC_PC_* */
+  int32_t sweeps;
+  int32_t cycles;
+  int32_t levels;
+  int32_t coarse_sweeps;
+} uc_precond_cfg;
+
+/* Sticky device-side status, read with uc_status (synchronises). */
+typedef struct uc_status_t {
+  int32_t residual_nonfinite;   /* a residual/Jv output entry was non-finite */
+  int32_t precond_nonfinite;    /* a preconditioner application was non-finite */
+  int32_t precond_bad_diag;     /* build: non-positive (fine) / zero (coarse) diagonal */
+  int32_t pad;
+} uc_status_t;
+
+int uc_abi_version(void);
+const char* uc_last_error(void);
+
+/* Create / destroy a context bound to the current device.  stream may be 0. */
+int uc_ctx_create(const uc_mesh_desc* mesh, const uc_model_params* params,
+                  void* cuda_stream, uc_ctx** out);
+int uc_ctx_destroy(uc_ctx* ctx);
+int uc_set_stream(uc_ctx* ctx, void* cuda_stream);
+int64_t uc_n_local(const uc_ctx* ctx);  /* owned nodes per field on this rank */
+
+/* Ghost node planes for slab-decomposed runs: device storage for one plane of
+ * both fields below (side 0) and above (side 1) the owned slab, per input
+ * slot (0 = u/new, 1 = old, 2 = prev, 3 = v).  The host fills them (NCCL
+ * send/recv) before a residual/Jv call.  NULL on a single GPU. */
+double* uc_ghost_ptr(uc_ctx* ctx, int slot, int side);
+
+/* assemble_residual(part="new"|"old") (assembly.py:214-230) restricted to the
+ * owned nodes, with the lagged rate (stepping.py:40-50) built on the fly.
+ *   part = UC_PART_OLD: out = old-level assembly (TimestepResidual.fixed_part,
+ *          assembly.py:256-258); `unew` is ignored.
+ *   part = UC_PART_NEW: out = new-level assembly + fixed (TimestepResidual.
+ *          __call__, assembly.py:261-268).
+ * A non-finite assembled entry sets residual_nonfinite. */
+int uc_residual(uc_ctx* ctx, const uc_scheme* sc, int part, const double* unew,
+                const double* old, const double* prev, const double* fixed,
+                double* out);
+
+/* Locate the first non-finite Gauss-point integrand like _check_finite
+ * (assembly.py:174-190).  Synchronises.  Writes field, part (0 value,
+ * 1+d flux[d]), element id, quadrature point and first node; returns 0 if
+ * every integrand is finite (fields set to -1). */
+int uc_locate_nonfinite(uc_ctx* ctx, const uc_scheme* sc, int part,
+                        const double* unew, const double* old, const double* prev,
+                        int64_t* field, int64_t* which, int64_t* element,
+                        int64_t* qp, int64_t* first_node);
+
+/* _FdOperator.__call__ / jfnk_matvec (newton.py:84-113):
+ *   jv = (F(u + eps v) - fu) / eps,  eps = sqrt(DBL_EPSILON)*sqrt(1+unorm)/|v|,
+ * with u + eps v formed on the fly inside the residual tile.  |v| is reduced
+ * on the device; jv = 0 if |v| == 0.  eps_out (device, may be NULL) receives eps
+ * (0 when |v| == 0). */
+int uc_jv(uc_ctx* ctx, const uc_scheme* sc, const double* u, const double* fu,
+          const double* v, double unorm, const double* old, const double* prev,
+          const double* fixed, double* jv, double* eps_out);
+
+/* Deterministic fixed-order reductions over n entries (np.dot / np.linalg.norm
+ * as used by newton.py and krylov.py).  Results go to device scalars. */
+int uc_dot(uc_ctx* ctx, int64_t n, const double* a, const double* b, double* out_dev);
+int uc_norm(uc_ctx* ctx, int64_t n, const double* a, double* out_dev);
+/* Host-returning variants (synchronise). */
+int uc_dot_host(uc_ctx* ctx, int64_t n, const double* a, const double* b, double* out);
+int uc_norm_host(uc_ctx* ctx, int64_t n, const double* a, double* out);
+
+/* arnoldi_step (krylov.py:48-70): MGS of w against basis[0..k] plus one full
+ * re-orthogonalisation pass, h[k+1] = |w|, and basis[k+1] = w / h[k+1] unless
+ * h[k+1] < 1e-14*scale (breakdown).  basis is an array of k+2 device pointers
+ * (basis[k+1] is the output slot).  Synchronises; h_host gets k+2 values,
+ * *broke the breakdown flag. */
+int uc_arnoldi(uc_ctx* ctx, int64_t n, const double* const* basis, int k,
+               double* w, double scale, double* h_host, int* broke);
+
+/* out = sum_j y[j] * basis[j], j = 0..k-1 (krylov.py:180-182 basis[:k].T @ y). */
+int uc_combine(uc_ctx* ctx, int64_t n, const double* const* basis, int k,
+               const double* y_host, double* out);
+
+/* Elementwise helpers used by the solver control flow (newton.py:164-165,
+ * krylov.py:124-131,183,191): out = a + s*b  (two roundings, numpy order). */
+int uc_axpy(uc_ctx* ctx, int64_t n, const double* a, double s, const double* b,
+            double* out);
+/* out = a - b */
+int uc_sub(uc_ctx* ctx, int64_t n, const double* a, const double* b, double* out);
+/* out = a / s */
+int uc_scale_div(uc_ctx* ctx, int64_t n, const double* a, double s, double* out);
+/* out = s * a */
+int uc_scale(uc_ctx* ctx, int64_t n, double s, const double* a, double* out);
+
+/* build_precond (precond.py:269-299): frozen Gauss-point state -> block
+ * coefficients (free_growth.py:223-231 / alloy.py:286-300) -> fixed 9/27-point
+ * stencils (assembly.py:271-303) -> Galerkin hierarchy (precond.py:191-206).
+ * Synchronises; returns UC_ERR_ARG with precond_bad_diag set on a
+ * non-positive diagonal. */
+int uc_precond_build(uc_ctx* ctx, const uc_scheme* sc, const double* state,
+                     const uc_precond_cfg* cfg);
+/* BlockPrecond.apply (precond.py:248-264), both field blocks per launch. */
+int uc_precond_apply(uc_ctx* ctx, const double* v, double* out);
+/* Copy the stencil of level/block to host: rows x 3^dim values in natural
+ * row order, offsets (dx,dy[,dz]) lexicographic with dx fastest. */
+int uc_precond_stencil(uc_ctx* ctx, int level, int block, double* host_out);
+int uc_precond_levels(uc_ctx* ctx, int64_t* shapes /* [levels][3] */);
+
+/* Sticky status flags (synchronises); clear=1 resets them. */
+int uc_status(uc_ctx* ctx, uc_status_t* out, int clear);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UC_B200_H */

@@ -1,0 +1,117 @@
+"""ctypes binding of the C ABI in include/uc_b200.h.
+
+This is the only place the shared library is loaded.  There is no fallback:
+if the library or a CUDA device is missing, every device entry point raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "_lib", "libuc_b200.so")
+
+UC_OK, UC_ERR_NONFINITE, UC_ERR_ARG, UC_ERR_CUDA, UC_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
+UC_MODEL_FREE_GROWTH, UC_MODEL_ALLOY = 1, 2
+UC_PART_NEW, UC_PART_OLD = 0, 1
+UC_PC_IDENTITY, UC_PC_JACOBI, UC_PC_SGS, UC_PC_VCYCLE = 0, 1, 2, 3
+
+
+class MeshDesc(C.Structure):
+    _fields_ = [("dim", C.c_int32), ("order", C.c_int32), ("counts", C.c_int64 * 3),
+                ("spacing", C.c_double * 3), ("slab_lo", C.c_int64), ("slab_hi", C.c_int64)]
+
+
+class ModelParams(C.Structure):
+    _fields_ = [("model", C.c_int32), ("normalized", C.c_int32), ("eps", C.c_double),
+                ("reg", C.c_double), ("aniso_reg_grad", C.c_double), ("bg", C.c_double),
+                ("beta", C.c_double), ("alpha", C.c_double), ("latent", C.c_double),
+                ("hcell", C.c_double), ("tmelt", C.c_double), ("at_reg2", C.c_double),
+                ("kpart", C.c_double), ("coupling", C.c_double), ("dcoef", C.c_double),
+                ("g4_coef", C.c_double), ("pull_velocity", C.c_double)]
+
+
+class Scheme(C.Structure):
+    _fields_ = [("theta", C.c_double), ("dt", C.c_double), ("step", C.c_int64)]
+
+
+class PrecondCfg(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("sweeps", C.c_int32), ("cycles", C.c_int32),
+                ("levels", C.c_int32), ("coarse_sweeps", C.c_int32)]
+
+
+class Status(C.Structure):
+    _fields_ = [("residual_nonfinite", C.c_int32), ("precond_nonfinite", C.c_int32),
+                ("precond_bad_diag", C.c_int32), ("pad", C.c_int32)]
+
+
+_P = C.c_void_p
+_D = C.c_double
+_I64 = C.c_int64
+_I = C.c_int
+
+# name -> (restype, argtypes); every symbol declared in include/uc_b200.h
+SIGNATURES = {
+    "uc_abi_version": (C.c_int, []),
+    "uc_last_error": (C.c_char_p, []),
+    "uc_ctx_create": (_I, [C.POINTER(MeshDesc), C.POINTER(ModelParams), _P, C.POINTER(_P)]),
+    "uc_ctx_destroy": (_I, [_P]),
+    "uc_set_stream": (_I, [_P, _P]),
+    "uc_n_local": (_I64, [_P]),
+    "uc_ghost_ptr": (_P, [_P, _I, _I]),
+    "uc_residual": (_I, [_P, C.POINTER(Scheme), _I, _P, _P, _P, _P, _P]),
+    "uc_locate_nonfinite": (_I, [_P, C.POINTER(Scheme), _I, _P, _P, _P] + [C.POINTER(_I64)] * 5),
+    "uc_jv": (_I, [_P, C.POINTER(Scheme), _P, _P, _P, _D, _P, _P, _P, _P, _P]),
+    "uc_dot": (_I, [_P, _I64, _P, _P, _P]),
+    "uc_norm": (_I, [_P, _I64, _P, _P]),
+    "uc_dot_host": (_I, [_P, _I64, _P, _P, C.POINTER(_D)]),
+    "uc_norm_host": (_I, [_P, _I64, _P, C.POINTER(_D)]),
+    "uc_arnoldi": (_I, [_P, _I64, C.POINTER(_P), _I, _P, _D, C.POINTER(_D), C.POINTER(_I)]),
+    "uc_combine": (_I, [_P, _I64, C.POINTER(_P), _I, C.POINTER(_D), _P]),
+    "uc_axpy": (_I, [_P, _I64, _P, _D, _P, _P]),
+    "uc_sub": (_I, [_P, _I64, _P, _P, _P]),
+    "uc_scale_div": (_I, [_P, _I64, _P, _D, _P]),
+    "uc_scale": (_I, [_P, _I64, _D, _P, _P]),
+    "uc_precond_build": (_I, [_P, C.POINTER(Scheme), _P, C.POINTER(PrecondCfg)]),
+    "uc_precond_apply": (_I, [_P, _P, _P]),
+    "uc_precond_stencil": (_I, [_P, _I, _I, _P]),
+    "uc_precond_levels": (_I, [_P, C.POINTER(_I64)]),
+    "uc_status": (_I, [_P, C.POINTER(Status), _I]),
+}
+
+_lock = threading.Lock()
+_lib = None
+
+
+class UcError(RuntimeError):
+    pass
+
+
+def load(path: str = LIB_PATH):
+    """Load the library (no CUDA needed for loading itself)."""
+    global _lib
+    with _lock:
+        if _lib is None:
+            if not os.path.exists(path):
+                raise UcError(
+                    f"B200 hot-path library not built: {path} is missing "
+                    "(run `python -m paper_2006_16764_b200.build`)")
+            lib = C.CDLL(path)
+            for name, (res, args) in SIGNATURES.items():
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def check(rc: int, what: str = "") -> None:
+    if rc != UC_OK:
+        msg = load().uc_last_error().decode(errors="replace")
+        raise UcError(f"{what}: {msg} (code {rc})")
+
+
+def ptr(t) -> C.c_void_p:
+    return C.c_void_p(t.data_ptr())

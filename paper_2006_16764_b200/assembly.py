@@ -1,0 +1,171 @@
+"""Residual assembly on the B200 (drop-in for undercool/assembly.py).
+
+``TimestepResidual`` keeps the reference's contract (assembly.py:233-268):
+the old-level part is assembled once at construction (``fixed_part``), each
+call returns a newly allocated F(u) = A_new(u) + fixed_part, ``evaluations``
+counts calls, inputs are never mutated, and a non-finite assembled entry
+raises NonFiniteResidualError naming the element and quadrature point.
+
+Vectors may be numpy arrays (copied to the device and back, for
+compatibility) or CUDA fp64 tensors (kept on the device).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .device import as_device, context_for, is_device, to_host
+from .errors import NonFiniteResidualError
+
+__all__ = ["StateHistory", "split_fields", "join_fields", "assemble_residual",
+           "TimestepResidual", "NonFiniteResidualError", "scheme_struct"]
+
+
+@dataclass
+class StateHistory:
+    new: object
+    old: object
+    prev: object
+
+
+def split_fields(u, n_fields: int):
+    return u.reshape(n_fields, -1)
+
+
+def join_fields(*fields):
+    if fields and isinstance(fields[0], torch.Tensor):
+        return torch.cat([f.reshape(-1).to(torch.float64) for f in fields])
+    return np.concatenate([np.asarray(f, dtype=float).reshape(-1) for f in fields])
+
+
+def scheme_struct(scheme) -> L.Scheme:
+    sc = L.Scheme()
+    sc.theta, sc.dt, sc.step = float(scheme.theta), float(scheme.dt), int(scheme.step)
+    return sc
+
+
+def _default_rule(rule) -> None:
+    if rule is None:
+        return
+    pts = rule[0] if isinstance(rule, tuple) else getattr(rule, "points", None)
+    if pts is None or len(pts) not in (9, 27):
+        raise NotImplementedError("the device path integrates with the 3-point Gauss rule only")
+
+
+def _raise_nonfinite(ctx, sc, part, u, old, prev):
+    f, w, e, q, first = (C.c_int64() for _ in range(5))
+    lib = ctx.lib
+    L.check(lib.uc_locate_nonfinite(
+        ctx.bind(), C.byref(sc), part, L.ptr(u) if u is not None else None, L.ptr(old), L.ptr(prev),
+        C.byref(f), C.byref(w), C.byref(e), C.byref(q), C.byref(first)), "uc_locate_nonfinite")
+    if f.value < 0:
+        raise NonFiniteResidualError("non-finite residual entry after assembly")
+    name = "value" if w.value == 0 else f"flux[{w.value - 1}]"
+    raise NonFiniteResidualError(
+        f"non-finite {name} integrand for field {f.value} at element {e.value} "
+        f"(first node {first.value}), quadrature point {q.value}")
+
+
+class TimestepResidual:
+    """Residual of one timestep as a function of the new state only."""
+
+    _uc_device = True
+
+    def __init__(self, mesh, kernel, old, prev, scheme, rule=None):
+        _default_rule(rule)
+        self.mesh = mesh
+        self.kernel = kernel
+        self.scheme = scheme
+        self.rule = rule
+        self.ctx = context_for(mesh, kernel)
+        self._host_io = not is_device(old)
+        self.old = as_device(old)
+        self.prev = as_device(prev)
+        self._sc = scheme_struct(scheme)
+        n2 = 2 * self.ctx.n_local
+        if self.old.numel() != n2 or self.prev.numel() != n2:
+            raise ValueError(f"state vectors must hold {n2} values")
+        fixed = torch.empty_like(self.old)
+        L.check(self.ctx.lib.uc_residual(self.ctx.bind(), C.byref(self._sc), L.UC_PART_OLD, None,
+                                         L.ptr(self.old), L.ptr(self.prev), None, L.ptr(fixed)),
+                "uc_residual(old)")
+        self._check(L.UC_PART_OLD, None)
+        self._fixed = fixed
+        self.evaluations = 0
+
+    @property
+    def fixed_part(self):
+        return to_host(self._fixed) if self._host_io else self._fixed
+
+    def _check(self, part, u):
+        st = self.ctx.status(clear=True)
+        if st.residual_nonfinite:
+            _raise_nonfinite(self.ctx, self._sc, part, u, self.old, self.prev)
+
+    def device_call(self, u: torch.Tensor, check: bool = True) -> torch.Tensor:
+        """F(u) for a device vector, result on the device."""
+        self.evaluations += 1
+        out = torch.empty_like(u)
+        L.check(self.ctx.lib.uc_residual(self.ctx.bind(), C.byref(self._sc), L.UC_PART_NEW, L.ptr(u),
+                                         L.ptr(self.old), L.ptr(self.prev), L.ptr(self._fixed),
+                                         L.ptr(out)), "uc_residual(new)")
+        if check:
+            self._check(L.UC_PART_NEW, u)
+        return out
+
+    def __call__(self, u_new):
+        if is_device(u_new):
+            return self.device_call(as_device(u_new))
+        return to_host(self.device_call(as_device(u_new)))
+
+    def jv_device(self, u, fu, v, unorm: float, eps_out=None) -> torch.Tensor:
+        """(F(u + eps v) - F(u)) / eps fused on the device (newton.py:107-113).
+        Non-finite F(u+eps v) sets the sticky flag checked by the caller."""
+        self.evaluations += 1
+        out = torch.empty_like(u)
+        L.check(self.ctx.lib.uc_jv(self.ctx.bind(), C.byref(self._sc), L.ptr(u), L.ptr(fu), L.ptr(v),
+                                   float(unorm), L.ptr(self.old), L.ptr(self.prev), L.ptr(self._fixed),
+                                   L.ptr(out), L.ptr(eps_out) if eps_out is not None else None),
+                "uc_jv")
+        return out
+
+
+def assemble_residual(mesh, kernel, states, scheme, rule=None, elements=None, part="full"):
+    """Global residual of one theta step (assembly.py:214-230) on the device.
+
+    part="old" is the fixed part, part="new" the live part, part="full" their
+    sum.  Element subsets are not supported on the device."""
+    if elements is not None:
+        raise NotImplementedError("element subsets are not assembled on the device")
+    _default_rule(rule)
+    ctx = context_for(mesh, kernel)
+    host = not is_device(states.old)
+    old, prev = as_device(states.old), as_device(states.prev)
+    sc = scheme_struct(scheme)
+    fixed = torch.empty_like(old)
+    L.check(ctx.lib.uc_residual(ctx.bind(), C.byref(sc), L.UC_PART_OLD, None, L.ptr(old),
+                                L.ptr(prev), None, L.ptr(fixed)), "uc_residual(old)")
+    if part == "old":
+        out = fixed
+        st = ctx.status()
+        if st.residual_nonfinite:
+            _raise_nonfinite(ctx, sc, L.UC_PART_OLD, None, old, prev)
+    else:
+        if part not in ("new", "full"):
+            raise ValueError(f"unknown part {part!r}")
+        if ctx.status().residual_nonfinite and part == "full":
+            _raise_nonfinite(ctx, sc, L.UC_PART_OLD, None, old, prev)
+        new = as_device(states.new)
+        zero = torch.zeros_like(old)
+        out = torch.empty_like(old)
+        L.check(ctx.lib.uc_residual(ctx.bind(), C.byref(sc), L.UC_PART_NEW, L.ptr(new), L.ptr(old),
+                                    L.ptr(prev), L.ptr(zero if part == "new" else fixed),
+                                    L.ptr(out)), "uc_residual(new)")
+        if ctx.status().residual_nonfinite:
+            _raise_nonfinite(ctx, sc, L.UC_PART_NEW, new, old, prev)
+    return to_host(out) if host else out

@@ -1,0 +1,301 @@
+// K3-K5: deterministic reductions and the GMRES Arnoldi vector operations.
+//
+// Replaces np.dot / np.linalg.norm (newton.py:89-104, krylov.py:110,125),
+// arnoldi_step (krylov.py:48-70: MGS + one full re-orthogonalisation pass) and
+// the basis combination basis[:k].T @ y (krylov.py:180-182).
+//
+// Reductions are two-level trees with a fixed shape (grid depends only on n):
+// each CTA reduces a grid-strided range in registers, then a warp-shuffle
+// tree, then the last CTA to finish (ticket counter) sums the per-CTA partials
+// in index order.  Results are bitwise reproducible run to run.
+//
+// MGS is kept exactly sequential (the reference's j-by-j order) but each
+// launch fuses "w -= h_j V_j" with the partial dot for the NEXT projection,
+// so a full Arnoldi step reads V_j, V_{j+1} and w once per projection.
+#include "uc_internal.h"
+
+namespace uc {
+
+static inline unsigned red_grid(int64_t n) {
+  int64_t b = (n + (int64_t)UC_RED_THREADS * 4 - 1) / ((int64_t)UC_RED_THREADS * 4);
+  if (b < 1) b = 1;
+  if (b > UC_RED_GRID_MAX) b = UC_RED_GRID_MAX;
+  return (unsigned)b;
+}
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0) {
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += sh[w];
+  }
+  __syncthreads();
+  return s;  // valid in thread 0
+}
+
+// Finish a reduction: thread 0 of every CTA holds its CTA sum `s`.  The last
+// CTA sums the partials in index order and writes *out (optionally sqrt).
+__device__ __forceinline__ void finish_reduce(double s, double* partials, unsigned int* ticket,
+                                              double* out, bool do_sqrt, double* sh) {
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    partials[blockIdx.x] = s;
+    __threadfence();
+    const unsigned t = atomicAdd(ticket, 1u);
+    last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double v = 0.0;
+  for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) v += __ldcg(partials + i);
+  const double tot = block_sum(v, sh);
+  if (threadIdx.x == 0) {
+    *out = do_sqrt ? sqrt(tot) : tot;
+    *ticket = 0u;
+  }
+}
+
+__global__ void __launch_bounds__(UC_RED_THREADS) k_dot(int64_t n, const double* __restrict__ a,
+                                                        const double* __restrict__ b,
+                                                        double* partials, unsigned int* ticket,
+                                                        double* out, int do_sqrt) {
+  __shared__ double sh[32];
+  double acc = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    acc += a[i] * (b ? b[i] : a[i]);
+  const double s = block_sum(acc, sh);
+  finish_reduce(s, partials, ticket, out, do_sqrt != 0, sh);
+}
+
+int reduce_dot(uc_ctx* c, int64_t n, const double* a, const double* b, double* out_dev,
+               bool sqrt_result) {
+  k_dot<<<red_grid(n), UC_RED_THREADS, 0, c->stream>>>(n, a, b, c->partials, c->ticket, out_dev,
+                                                       sqrt_result ? 1 : 0);
+  UC_CUDA_OK(cudaGetLastError());
+  return UC_OK;
+}
+
+// One MGS projection: s = *s_in; w -= s*Vj; h[j] (=|+=) s; next dot partial.
+__global__ void __launch_bounds__(UC_RED_THREADS)
+    k_mgs(int64_t n, const double* __restrict__ vj, double* __restrict__ w,
+          const double* __restrict__ vnext, const double* s_in, double* h_j, int accumulate,
+          double* partials, unsigned int* ticket, double* s_out, int do_sqrt) {
+  __shared__ double sh[32];
+  const double s = *s_in;
+  if (blockIdx.x == 0 && threadIdx.x == 0) *h_j = accumulate ? *h_j + s : s;
+  double acc = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    // w = w - hj * basis[j]  (krylov.py:62,66): two roundings
+    const double wi = __dsub_rn(w[i], __dmul_rn(s, vj[i]));
+    w[i] = wi;
+    acc += (vnext ? vnext[i] : wi) * wi;
+  }
+  const double t = block_sum(acc, sh);
+  finish_reduce(t, partials, ticket, s_out, do_sqrt != 0, sh);
+}
+
+// basis[k+1] = w / h[k+1] unless breakdown (krylov.py:67-70)
+__global__ void k_normalize(int64_t n, const double* __restrict__ w, const double* hk1,
+                            double tol, double* __restrict__ out) {
+  const double h = *hk1;
+  if (!(h >= tol)) return;  // breakdown (or NaN): host ignores the slot
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = __ddiv_rn(w[i], h);
+}
+
+#define UC_COMBINE_MAX 48
+struct CombineArgs {
+  const double* v[UC_COMBINE_MAX];
+  double y[UC_COMBINE_MAX];
+  int k;
+  int accumulate;
+};
+
+__global__ void k_combine(int64_t n, const CombineArgs a, double* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    double s = a.accumulate ? out[i] : 0.0;
+    for (int j = 0; j < a.k; ++j) s += a.y[j] * __ldg(a.v[j] + i);
+    out[i] = s;
+  }
+}
+
+__global__ void k_axpy(int64_t n, const double* __restrict__ a, double s,
+                       const double* __restrict__ b, double* __restrict__ out, int op) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    double r;
+    if (op == 0)
+      r = __dadd_rn(a[i], __dmul_rn(s, b[i]));  // a + s*b
+    else if (op == 1)
+      r = __dsub_rn(a[i], b[i]);  // a - b
+    else if (op == 2)
+      r = __ddiv_rn(a[i], s);  // a / s
+    else
+      r = __dmul_rn(s, a[i]);  // s*a
+    out[i] = r;
+  }
+}
+
+__global__ void k_nonfinite(int64_t n, const double* __restrict__ a, unsigned int* flag) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  bool bad = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    bad |= !isfinite(a[i]);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
+static inline unsigned ew_grid(uc_ctx* c, int64_t n) {
+  int64_t b = (n + 255) / 256;
+  const int64_t cap = (int64_t)c->num_sms * 16;
+  if (b > cap) b = cap;
+  if (b < 1) b = 1;
+  return (unsigned)b;
+}
+
+int launch_axpy(uc_ctx* c, int64_t n, const double* a, double s, const double* b, double* out) {
+  k_axpy<<<ew_grid(c, n), 256, 0, c->stream>>>(n, a, s, b, out, 0);
+  UC_CUDA_OK(cudaGetLastError());
+  return UC_OK;
+}
+
+int nonfinite_flag(uc_ctx* c, int64_t n, const double* a, unsigned int* flag) {
+  k_nonfinite<<<ew_grid(c, n), 256, 0, c->stream>>>(n, a, flag);
+  UC_CUDA_OK(cudaGetLastError());
+  return UC_OK;
+}
+
+}  // namespace uc
+
+using namespace uc;
+
+extern "C" {
+
+int uc_dot(uc_ctx* c, int64_t n, const double* a, const double* b, double* out_dev) {
+  if (!c || n < 0) return set_error(UC_ERR_ARG, "uc_dot: bad argument");
+  if (n == 0) {
+    UC_CUDA_OK(cudaMemsetAsync(out_dev, 0, sizeof(double), c->stream));
+    return UC_OK;
+  }
+  return reduce_dot(c, n, a, b, out_dev, false);
+}
+
+int uc_norm(uc_ctx* c, int64_t n, const double* a, double* out_dev) {
+  if (!c || n < 0) return set_error(UC_ERR_ARG, "uc_norm: bad argument");
+  if (n == 0) {
+    UC_CUDA_OK(cudaMemsetAsync(out_dev, 0, sizeof(double), c->stream));
+    return UC_OK;
+  }
+  return reduce_dot(c, n, a, nullptr, out_dev, true);
+}
+
+int uc_dot_host(uc_ctx* c, int64_t n, const double* a, const double* b, double* out) {
+  int rc = uc_dot(c, n, a, b, c->scal);
+  if (rc) return rc;
+  UC_CUDA_OK(cudaMemcpyAsync(c->pinned, c->scal, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  UC_CUDA_OK(cudaStreamSynchronize(c->stream));
+  *out = c->pinned[0];
+  return UC_OK;
+}
+
+int uc_norm_host(uc_ctx* c, int64_t n, const double* a, double* out) {
+  int rc = uc_norm(c, n, a, c->scal);
+  if (rc) return rc;
+  UC_CUDA_OK(cudaMemcpyAsync(c->pinned, c->scal, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+  UC_CUDA_OK(cudaStreamSynchronize(c->stream));
+  *out = c->pinned[0];
+  return UC_OK;
+}
+
+int uc_arnoldi(uc_ctx* c, int64_t n, const double* const* basis, int k, double* w, double scale,
+               double* h_host, int* broke) {
+  if (!c || !basis || !w || k < 0 || 3 * (k + 2) + 8 > UC_SCAL_SLOTS)
+    return set_error(UC_ERR_ARG, "uc_arnoldi: bad argument (k=%d)", k);
+  // scalar layout: [0, k+2) h; then 2(k+1)+1 dot slots
+  double* h = c->scal;
+  double* slots = c->scal + (k + 2);
+  const int m = 2 * (k + 1);
+  int rc = reduce_dot(c, n, basis[0], w, &slots[0], false);
+  if (rc) return rc;
+  const unsigned grid = red_grid(n);
+  for (int t = 0; t < m; ++t) {
+    const int j = t % (k + 1);
+    const bool last = (t + 1 == m);
+    const double* vnext = last ? nullptr : basis[(t + 1) % (k + 1)];
+    k_mgs<<<grid, UC_RED_THREADS, 0, c->stream>>>(n, basis[j], w, vnext, &slots[t], &h[j],
+                                                  t >= k + 1 ? 1 : 0, c->partials, c->ticket,
+                                                  last ? &h[k + 1] : &slots[t + 1], last ? 1 : 0);
+    UC_CUDA_OK(cudaGetLastError());
+  }
+  const double tol = 1e-14 * scale;  // BREAKDOWN_TOL * scale (krylov.py:13,67)
+  k_normalize<<<ew_grid(c, n), 256, 0, c->stream>>>(n, w, &h[k + 1], tol,
+                                                    const_cast<double*>(basis[k + 1]));
+  UC_CUDA_OK(cudaGetLastError());
+  UC_CUDA_OK(cudaMemcpyAsync(c->pinned, h, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost,
+                             c->stream));
+  UC_CUDA_OK(cudaStreamSynchronize(c->stream));
+  for (int i = 0; i < k + 2; ++i) h_host[i] = c->pinned[i];
+  *broke = (h_host[k + 1] < tol) ? 1 : 0;
+  return UC_OK;
+}
+
+int uc_combine(uc_ctx* c, int64_t n, const double* const* basis, int k, const double* y,
+               double* out) {
+  if (!c || k < 0) return set_error(UC_ERR_ARG, "uc_combine: bad argument");
+  if (k == 0) {
+    UC_CUDA_OK(cudaMemsetAsync(out, 0, sizeof(double) * n, c->stream));
+    return UC_OK;
+  }
+  for (int j0 = 0; j0 < k; j0 += UC_COMBINE_MAX) {
+    CombineArgs a{};
+    a.k = (k - j0) < UC_COMBINE_MAX ? (k - j0) : UC_COMBINE_MAX;
+    a.accumulate = j0 > 0;
+    for (int j = 0; j < a.k; ++j) {
+      a.v[j] = basis[j0 + j];
+      a.y[j] = y[j0 + j];
+    }
+    k_combine<<<ew_grid(c, n), 256, 0, c->stream>>>(n, a, out);
+    UC_CUDA_OK(cudaGetLastError());
+  }
+  return UC_OK;
+}
+
+int uc_axpy(uc_ctx* c, int64_t n, const double* a, double s, const double* b, double* out) {
+  if (!c || n < 0) return set_error(UC_ERR_ARG, "uc_axpy: bad argument");
+  if (n == 0) return UC_OK;
+  return launch_axpy(c, n, a, s, b, out);
+}
+
+int uc_sub(uc_ctx* c, int64_t n, const double* a, const double* b, double* out) {
+  if (!c || n < 0) return set_error(UC_ERR_ARG, "uc_sub: bad argument");
+  if (n == 0) return UC_OK;
+  k_axpy<<<ew_grid(c, n), 256, 0, c->stream>>>(n, a, 0.0, b, out, 1);
+  UC_CUDA_OK(cudaGetLastError());
+  return UC_OK;
+}
+
+int uc_scale_div(uc_ctx* c, int64_t n, const double* a, double s, double* out) {
+  if (!c || n < 0) return set_error(UC_ERR_ARG, "uc_scale_div: bad argument");
+  if (n == 0) return UC_OK;
+  k_axpy<<<ew_grid(c, n), 256, 0, c->stream>>>(n, a, s, nullptr, out, 2);
+  UC_CUDA_OK(cudaGetLastError());
+  return UC_OK;
+}
+
+int uc_scale(uc_ctx* c, int64_t n, double s, const double* a, double* out) {
+  if (!c || n < 0) return set_error(UC_ERR_ARG, "uc_scale: bad argument");
+  if (n == 0) return UC_OK;
+  k_axpy<<<ew_grid(c, n), 256, 0, c->stream>>>(n, a, s, nullptr, out, 3);
+  UC_CUDA_OK(cudaGetLastError());
+  return UC_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,76 @@
+// Internal host-side declarations shared by the translation units.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "uc_common.cuh"
+
+namespace uc {
+
+// Per-level physics constants, derived on the host exactly as the numba
+// prologues derive them (free_growth.py:97-108, alloy.py:137-147).
+struct LevelConsts {
+  double base, four_eps, eps32, reg, avg, avg_reg;
+  double inv_dt_s;  // mass_sign / dt
+  // free growth
+  double well_c, drive_c, wbg, half_w, walpha, tmelt, latent;
+  // alloy
+  double weight, inv_dt, coupling, omk, half_k, half_omk, dq_c, at_coef, at_reg2, g4_coef,
+      g4_shift;
+  int normalized;
+};
+
+LevelConsts make_level(const uc_model_params& p, int dim, const uc_scheme& sc, bool new_level);
+void make_jxw(const Grid& g, double* jxw);  // 9 or 27 entries, mesh.py:52-61,174-176
+
+struct Precond;  // precond.cu
+
+}  // namespace uc
+
+// Reduction geometry: fixed so the summation tree depends on n only.
+#define UC_RED_THREADS 256
+#define UC_RED_GRID_MAX 1184
+#define UC_SCAL_SLOTS 2048
+
+struct uc_ctx {
+  uc::Grid grid;
+  uc_mesh_desc mesh;
+  uc_model_params params;
+  cudaStream_t stream = nullptr;
+  int device = 0;
+  int num_sms = 148;
+  // reduction workspace
+  double* partials = nullptr;    // [UC_RED_GRID_MAX]
+  unsigned int* ticket = nullptr;
+  double* scal = nullptr;        // [UC_SCAL_SLOTS] device scalars
+  double* pinned = nullptr;      // [UC_SCAL_SLOTS] pinned host staging
+  unsigned int* flags = nullptr; // [4] sticky status flags
+  unsigned long long* locate_key = nullptr;
+  // ghost planes [slot][side] -> [2][plane]
+  double* ghost[4][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
+  uc::Precond* pc = nullptr;
+};
+
+namespace uc {
+// blas.cu
+int reduce_dot(uc_ctx* c, int64_t n, const double* a, const double* b, double* out_dev,
+               bool sqrt_result);
+int nonfinite_flag(uc_ctx* c, int64_t n, const double* a, unsigned int* flag);
+int launch_axpy(uc_ctx* c, int64_t n, const double* a, double s, const double* b, double* out);
+// residual.cu
+enum { MODE_NEW = 0, MODE_OLD = 1, MODE_JV = 2 };
+int launch_residual(uc_ctx* c, const uc_scheme* sc, int mode, const double* u,
+                    const double* old, const double* prev, const double* v, const double* fu,
+                    const double* fixed, double* out, double eps_num, const double* vnorm_dev,
+                    double* eps_out);
+int locate_nonfinite(uc_ctx* c, const uc_scheme* sc, int part, const double* u,
+                     const double* old, const double* prev, int64_t out[5]);
+// precond.cu
+int precond_build(uc_ctx* c, const uc_scheme* sc, const double* state, const uc_precond_cfg* cfg);
+int precond_apply(uc_ctx* c, const double* v, double* out);
+int precond_stencil(uc_ctx* c, int level, int block, double* host_out);
+int precond_levels(uc_ctx* c, int64_t* shapes);
+void precond_destroy(Precond* p);
+}  // namespace uc

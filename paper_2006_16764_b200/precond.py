@@ -1,0 +1,167 @@
+"""Block-diagonal preconditioner on the B200 (drop-in for undercool/precond.py).
+
+``build_precond`` freezes the time-level-n state, evaluates the per-block
+coefficients at Gauss points and fills fixed 9-/27-point stencils on the device
+(csrc/precond.cu K6), then builds the Galerkin hierarchy P^T A P (K7).
+``BlockPrecond.apply`` runs the multicolor symmetric Gauss-Seidel V-cycle
+(K8-K10) for both field blocks in each launch.
+
+Ordering.  The reference's default smoother ordering is "lexicographic"
+(precond.py:62), a sequential triangular sweep.  The device implements the
+reference's own "multicolor" ordering (precond.py:113-121) exactly; for
+ordering="lexicographic" it warns once and applies multicolor (identical
+Newton/GMRES counts on every case measured).  Set
+UC_B200_STRICT_ORDERING=1 to raise instead.  kind="direct" (SuperLU) has no
+device implementation and raises.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import warnings
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from . import device as D
+from .assembly import scheme_struct
+
+__all__ = ["PrecondConfig", "BlockPrecond", "build_precond", "apply_precond"]
+
+_KINDS = {"identity": L.UC_PC_IDENTITY, "jacobi": L.UC_PC_JACOBI, "sgs": L.UC_PC_SGS,
+          "vcycle": L.UC_PC_VCYCLE}
+_warned = False
+
+
+@dataclass
+class PrecondConfig:
+    enabled: bool = True
+    kind: str = "vcycle"
+    sweeps: int = 2
+    cycles: int = 2
+    levels: int = 4
+    coarse_sweeps: int = 10
+    ordering: str = "lexicographic"
+    rebuild: str = "step"
+
+    def __post_init__(self):
+        if self.kind not in ("identity", "jacobi", "sgs", "vcycle", "direct"):
+            raise ValueError(f"unknown preconditioner kind '{self.kind}'")
+        if self.ordering not in ("multicolor", "lexicographic"):
+            raise ValueError(f"unknown ordering '{self.ordering}'")
+        if self.rebuild not in ("step", "newton"):
+            raise ValueError(f"unknown rebuild policy '{self.rebuild}'")
+
+
+def _stencil_to_csr(st: np.ndarray, shape, dim):
+    """Natural-order stencil rows -> scipy CSR (for inspection only)."""
+    import scipy.sparse as sp
+
+    n = int(np.prod(shape[:dim]))
+    rows, cols, vals = [], [], []
+    idx = np.arange(n)
+    coords = [(idx // int(np.prod(shape[:a]))) % shape[a] for a in range(dim)]
+    k = 0
+    for dz in ((-1, 0, 1) if dim == 3 else (0,)):
+        for dy in (-1, 0, 1):
+            for dx in (-1, 0, 1):
+                off = (dx, dy, dz)[:dim]
+                ok = np.ones(n, dtype=bool)
+                j = idx.copy()
+                stride = 1
+                for a in range(dim):
+                    ok &= (coords[a] + off[a] >= 0) & (coords[a] + off[a] < shape[a])
+                    j = j + off[a] * stride
+                    stride *= shape[a]
+                rows.append(idx[ok])
+                cols.append(j[ok])
+                vals.append(st[ok, k])
+                k += 1
+    return sp.csr_matrix((np.concatenate(vals), (np.concatenate(rows), np.concatenate(cols))),
+                         shape=(n, n))
+
+
+class _BlockView:
+    """Read-only view of one field block's level hierarchy (host copies)."""
+
+    def __init__(self, pc, block):
+        self._pc = pc
+        self._block = block
+
+    @property
+    def mats(self):
+        return [self._pc.level_matrix(lvl, self._block) for lvl in range(self._pc.n_levels)]
+
+
+class BlockPrecond:
+    _uc_device = True
+
+    def __init__(self, ctx, n_nodes: int, cfg: PrecondConfig, dim: int):
+        self._ctx = ctx
+        self.n_nodes = n_nodes
+        self.cfg = cfg
+        self.dim = dim
+        self.applications = 0
+        self.solvers = [_BlockView(self, 0), _BlockView(self, 1)]
+        shapes = (C.c_int64 * 24)()
+        self.n_levels = int(ctx.lib.uc_precond_levels(ctx.h, shapes))
+        self.level_shapes = [tuple(shapes[3 * l + a] for a in range(dim)) for l in range(self.n_levels)]
+
+    def level_stencil(self, level: int, block: int) -> np.ndarray:
+        shape = self.level_shapes[level]
+        out = np.empty((int(np.prod(shape)), 3 ** self.dim))
+        L.check(self._ctx.lib.uc_precond_stencil(self._ctx.bind(), level, block,
+                                                 out.ctypes.data_as(C.c_void_p)),
+                "uc_precond_stencil")
+        return out
+
+    def level_matrix(self, level: int, block: int):
+        return _stencil_to_csr(self.level_stencil(level, block), self.level_shapes[level], self.dim)
+
+    def device_apply(self, v: torch.Tensor, check: bool = True) -> torch.Tensor:
+        self.applications += 1
+        out = torch.empty_like(v)
+        L.check(self._ctx.lib.uc_precond_apply(self._ctx.bind(), L.ptr(v), L.ptr(out)),
+                "uc_precond_apply")
+        if check and self._ctx.status(clear=True).precond_nonfinite:
+            raise FloatingPointError("preconditioner produced non-finite values")
+        return out
+
+    def apply(self, v):
+        if D.is_device(v):
+            return self.device_apply(D.as_device(v))
+        return D.to_host(self.device_apply(D.as_device(v)))
+
+    __call__ = apply
+
+
+def build_precond(mesh, kernel, state, scheme, config: PrecondConfig | None = None) -> BlockPrecond:
+    global _warned
+    cfg = config or PrecondConfig()
+    if cfg.kind == "direct":
+        raise NotImplementedError("kind='direct' (SuperLU) has no device implementation")
+    if cfg.ordering == "lexicographic" and cfg.kind in ("sgs", "vcycle"):
+        if os.environ.get("UC_B200_STRICT_ORDERING") == "1":
+            raise NotImplementedError("lexicographic Gauss-Seidel is not implemented on the device")
+        if not _warned:
+            warnings.warn("ordering='lexicographic' is applied as the reference's multicolor "
+                          "ordering on the device", RuntimeWarning, stacklevel=2)
+            _warned = True
+    ctx = D.context_for(mesh, kernel, fresh=True)
+    st = D.as_device(state)
+    pc = L.PrecondCfg()
+    pc.kind = _KINDS[cfg.kind]
+    pc.sweeps, pc.cycles, pc.levels, pc.coarse_sweeps = cfg.sweeps, cfg.cycles, cfg.levels, cfg.coarse_sweeps
+    sc = scheme_struct(scheme)
+    rc = ctx.lib.uc_precond_build(ctx.bind(), C.byref(sc), L.ptr(st), C.byref(pc))
+    if rc == L.UC_ERR_ARG:
+        raise ValueError(ctx.lib.uc_last_error().decode())
+    L.check(rc, "uc_precond_build")
+    return BlockPrecond(ctx, ctx.n_local, cfg, mesh.dim)
+
+
+def apply_precond(precond: BlockPrecond, v):
+    return precond.apply(v)

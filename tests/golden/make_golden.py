@@ -1,0 +1,247 @@
+"""Generate golden input/output vectors by running the REFERENCE implementation.
+
+This script is test infrastructure: it imports the reference package
+(`undercool`, /root/reference/pkg/src) in this container, evaluates the hot-path
+functions on small seeded inputs and writes the results under tests/golden/.
+The GPU box has no /root/reference, so the committed .npz/.json files are what
+the tests read there.  Re-run with:
+
+    NUMBA_CACHE_DIR=/tmp/nbcache python tests/golden/make_golden.py
+
+Reference entry points exercised (file:line under /root/reference/pkg/src/undercool):
+  assemble_residual            assembly.py:214
+  TimestepResidual             assembly.py:233-268
+  jfnk_matvec                  newton.py:84-94
+  assemble_field_matrix        assembly.py:271-303
+  build_precond / apply        precond.py:269-299, 248-264
+  gmres_solve                  krylov.py:81-208
+  newton_solve                 newton.py:116-198
+  simulate (iteration counts)  driver.py:135-242
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import time
+
+os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/nbcache")
+REF = os.environ.get("UC_REFERENCE_SRC", "/root/reference/pkg/src")
+sys.path.insert(0, REF)
+
+import numpy as np  # noqa: E402
+
+import undercool as uc  # noqa: E402
+from undercool.assembly import StateHistory, assemble_residual  # noqa: E402
+from undercool.config import default_config  # noqa: E402
+from undercool.driver import simulate  # noqa: E402
+from undercool.models.alloy import AlloyParams, directional_initial_condition  # noqa: E402
+from undercool.models.free_growth import seed_initial_condition  # noqa: E402
+from undercool.newton import _FdOperator  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def fg_state(rng, n):
+    # distribution of tests/test_free_growth.py:246-256
+    return uc.join_fields(0.5 + 0.3 * rng.standard_normal(n), 1.0 + 0.2 * rng.standard_normal(n))
+
+
+def alloy_state(rng, n):
+    # distribution of tests/test_alloy.py:286-295
+    return uc.join_fields(np.tanh(rng.standard_normal(n)), -0.5 + 0.4 * rng.standard_normal(n))
+
+
+RESIDUAL_CASES = [
+    # name, model, dim, extents, counts, theta, dt, step, normalized
+    ("fg2d", "free_growth", 2, (0.48, 0.36), (16, 12), 0.5, 3e-4, 2, True),
+    ("fg3d", "free_growth", 3, (0.24, 0.18, 0.15), (8, 6, 5), 0.5, 3e-4, 2, True),
+    ("al2d", "alloy", 2, (6.4, 4.8), (8, 6), 0.5, 0.002, 7, True),
+    ("al2d_unnorm", "alloy", 2, (6.4, 4.8), (8, 6), 0.5, 0.002, 7, False),
+    ("al3d", "alloy", 3, (4.8, 3.2, 2.4), (6, 4, 3), 0.5, 0.002, 7, True),
+    ("fg2d_be", "free_growth", 2, (0.48, 0.36), (16, 12), 1.0, 2.25e-4, 0, True),
+]
+
+
+def kernel_for(model, normalized=True):
+    if model == "free_growth":
+        return uc.FreeGrowthKernel()
+    return uc.AlloyKernel(AlloyParams(antitrapping_normalized=normalized))
+
+
+def residual_cases(meta):
+    for name, model, dim, ext, cnt, th, dt, step, norm in RESIDUAL_CASES:
+        mesh = uc.build_mesh(dim, ext, cnt)
+        k = kernel_for(model, norm)
+        n = mesh.n_nodes
+        rng = np.random.default_rng(11 if model == "free_growth" else 12)
+        mk = fg_state if model == "free_growth" else alloy_state
+        new, old, prev = mk(rng, n), mk(rng, n), mk(rng, n)
+        scheme = uc.ThetaScheme(th, dt, step)
+        st = StateHistory(new, old, prev)
+        f_full = assemble_residual(mesh, k, st, scheme, part="full")
+        f_new = assemble_residual(mesh, k, st, scheme, part="new")
+        res = uc.TimestepResidual(mesh, k, old, prev, scheme)
+        f_call = res(new)
+        v = np.random.default_rng(2).standard_normal(2 * n)
+        op = _FdOperator(res, new, f_call)
+        jv = op(v)
+        jv2 = uc.jfnk_matvec(res, new, f_call, v)
+        np.savez_compressed(
+            os.path.join(OUT, f"residual_{name}.npz"),
+            new=new, old=old, prev=prev, v=v,
+            f_full=f_full, f_new=f_new, fixed=res.fixed_part, f_call=f_call,
+            jv=jv, jv_matvec=jv2, eps=np.array(op.epsilons),
+        )
+        meta[f"residual_{name}"] = dict(model=model, dim=dim, extents=ext, counts=cnt,
+                                         theta=th, dt=dt, step=step, normalized=norm)
+
+
+PRECOND_CASES = [
+    # name, model, dim, extents, counts, theta, dt, step
+    ("fg2d", "free_growth", 2, (0.96, 0.48), (32, 16), 0.5, 2.25e-4, 3),
+    ("fg3d", "free_growth", 3, (0.48, 0.24, 0.24), (16, 8, 8), 0.5, 2.25e-4, 3),
+    ("al2d", "alloy", 2, (25.6, 12.8), (32, 16), 0.5, 0.002, 3),
+    ("al3d", "alloy", 3, (12.8, 6.4, 6.4), (16, 8, 8), 0.5, 0.002, 3),
+]
+
+
+def precond_cases(meta):
+    for name, model, dim, ext, cnt, th, dt, step in PRECOND_CASES:
+        mesh = uc.build_mesh(dim, ext, cnt)
+        k = kernel_for(model)
+        n = mesh.n_nodes
+        rng = np.random.default_rng(11 if model == "free_growth" else 12)
+        if model == "free_growth":
+            state = fg_state(rng, n)
+        else:
+            # solute kept above -1/(1-k) so the phase-block mass stays positive
+            state = uc.join_fields(np.tanh(rng.standard_normal(n)),
+                                   np.clip(-0.5 + 0.3 * rng.standard_normal(n), -1.0, 0.9))
+        scheme = uc.ThetaScheme(th, dt, step)
+        v = np.random.default_rng(2).standard_normal(2 * n)
+        out = dict(state=state, v=v)
+        qs = uc.assembly.frozen_quad_state(mesh, k, state, scheme)
+        coeffs = k.precond_coefficients(qs, scheme)
+        for b, (cm, cd) in enumerate(coeffs):
+            mat = uc.assemble_field_matrix(mesh, cm, cd).tocsr()
+            mat.sort_indices()
+            out[f"A{b}_data"] = mat.data
+            out[f"A{b}_indices"] = mat.indices
+            out[f"A{b}_indptr"] = mat.indptr
+        for kind in ("identity", "jacobi", "sgs", "vcycle"):
+            cfg = uc.PrecondConfig(kind=kind, ordering="multicolor")
+            pc = uc.build_precond(mesh, k, state, scheme, cfg)
+            out[f"apply_{kind}"] = pc.apply(v)
+            if kind == "vcycle":
+                sizes = [m.shape[0] for m in pc.solvers[0].mats]
+                for lvl, m in enumerate(pc.solvers[0].mats[1:], start=1):
+                    for b in range(2):
+                        mm = pc.solvers[b].mats[lvl].tocsr()
+                        mm.sort_indices()
+                        out[f"L{lvl}_A{b}_data"] = mm.data
+                        out[f"L{lvl}_A{b}_indices"] = mm.indices
+                        out[f"L{lvl}_A{b}_indptr"] = mm.indptr
+        # non-default V-cycle settings
+        cfg = uc.PrecondConfig(kind="vcycle", ordering="multicolor", sweeps=1, cycles=1,
+                               levels=2, coarse_sweeps=3)
+        out["apply_vcycle_small"] = uc.build_precond(mesh, k, state, scheme, cfg).apply(v)
+        np.savez_compressed(os.path.join(OUT, f"precond_{name}.npz"), **out)
+        meta[f"precond_{name}"] = dict(model=model, dim=dim, extents=ext, counts=cnt,
+                                        theta=th, dt=dt, step=step, levels=sizes)
+
+
+def newton_case(meta):
+    """One preconditioned Newton solve (first step of a seed run)."""
+    mesh = uc.build_mesh(2, (0.96, 0.96), (32, 32))
+    k = uc.FreeGrowthKernel()
+    u0 = seed_initial_condition(mesh, k.params, radius=0.3)
+    scheme = uc.ThetaScheme(1.0, 2.25e-4, 0)
+    pc = uc.build_precond(mesh, k, u0, scheme, uc.PrecondConfig(ordering="multicolor"))
+    res = uc.TimestepResidual(mesh, k, u0, u0.copy(), scheme)
+    u, rep = uc.newton_solve(res, u0, uc.NewtonConfig(), precond_apply=pc.apply)
+    f0 = res(u0)
+    op = _FdOperator(res, u0, f0)
+    lin = uc.gmres_solve(op, -f0, tol=0.1, apply_minv=pc.apply)
+    np.savez_compressed(os.path.join(OUT, "newton_fg2d_32.npz"), u0=u0, u=u, f0=f0,
+                        gmres_x=lin.x, norms=np.array(rep.residual_norms))
+    meta["newton_fg2d_32"] = dict(iterations=rep.iterations, gmres=rep.gmres_iterations,
+                                  converged=bool(rep.converged), step_lengths=[float(x) for x in rep.step_lengths],
+                                  gmres_first=dict(iterations=lin.iterations,
+                                                   converged=bool(lin.converged),
+                                                   residual_norm=float(lin.residual_norm),
+                                                   cycles=lin.cycles,
+                                                   precond_applies=lin.precond_applies))
+
+
+RUNS = [
+    # name, model, dim, extents, counts, dt, t_final(steps), extra overrides
+    ("fg2d_128_10", "free_growth", 2, (3.84, 3.84), (128, 128), 2.25e-4, 10, {}, True),
+    ("fg2d_128_10_nopc", "free_growth", 2, (3.84, 3.84), (128, 128), 2.25e-4, 10,
+     {"enabled": False}, False),
+    ("al2d_256x64_10", "alloy", 2, (204.8, 51.2), (256, 64), 0.002, 10, {}, True),
+    ("fg3d_16_3", "free_growth", 3, (0.48, 0.48, 0.48), (16, 16, 16), 2.25e-4, 3, {}, True),
+    ("al3d_32x16x16_3", "alloy", 3, (25.6, 12.8, 12.8), (32, 16, 16), 0.002, 3, {}, True),
+]
+
+
+def run_cases(meta):
+    for name, model, dim, ext, cnt, dt, nsteps, pc_over, keep in RUNS:
+        cfg = default_config(model)
+        cfg.mesh.dimension = dim
+        cfg.mesh.extents = ext
+        cfg.mesh.counts = cnt
+        cfg.time.dt = dt
+        cfg.time.t_final = dt * nsteps
+        cfg.precond.ordering = "multicolor"
+        for key, val in pc_over.items():
+            setattr(cfg.precond, key, val)
+        t0 = time.perf_counter()
+        res = simulate(cfg)
+        wall = time.perf_counter() - t0
+        recs = res.records
+        meta[f"run_{name}"] = dict(
+            model=model, dim=dim, extents=ext, counts=cnt, dt=dt, steps=nsteps,
+            precond=pc_over, status=res.status,
+            newton=[r["newton_iters"] for r in recs],
+            gmres=[r["gmres_iters"] for r in recs],
+            fnorm=[float(r["fnorm"]) for r in recs],
+            fnorm0=[float(r["fnorm0"]) for r in recs],
+            theta=cfg.time.theta, startup_steps=cfg.time.startup_steps,
+            startup_dt=cfg.time.startup_dt, wall_seconds=wall,
+        )
+        if keep:
+            np.savez_compressed(os.path.join(OUT, f"run_{name}.npz"), state=res.state)
+        print(name, meta[f"run_{name}"]["newton"], meta[f"run_{name}"]["gmres"],
+              f"{wall:.1f}s", flush=True)
+
+
+def ic_cases(meta):
+    mesh = uc.build_mesh(2, (204.8, 51.2), (256, 64))
+    p = AlloyParams()
+    ic = directional_initial_condition(mesh, p, amplitude=0.5, seed=0, smooth=True)
+    mesh2 = uc.build_mesh(2, (3.84, 3.84), (128, 128))
+    seed = seed_initial_condition(mesh2, uc.FreeGrowthParams())
+    np.savez_compressed(os.path.join(OUT, "ic.npz"), alloy_256x64=ic, seed_128=seed)
+    meta["ic"] = dict(alloy=dict(extents=(204.8, 51.2), counts=(256, 64)),
+                      seed=dict(extents=(3.84, 3.84), counts=(128, 128)))
+
+
+def main():
+    meta = {"generator": "tests/golden/make_golden.py", "reference": REF}
+    residual_cases(meta)
+    precond_cases(meta)
+    newton_case(meta)
+    ic_cases(meta)
+    if "--no-runs" not in sys.argv:
+        run_cases(meta)
+    else:
+        old = json.load(open(os.path.join(OUT, "golden.json")))
+        meta.update({k: v for k, v in old.items() if k.startswith("run_")})
+    with open(os.path.join(OUT, "golden.json"), "w") as fh:
+        json.dump(meta, fh, indent=1, sort_keys=True)
+
+
+if __name__ == "__main__":
+    main()

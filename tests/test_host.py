@@ -1,0 +1,102 @@
+"""CPU-only checks: the C-ABI library loads and exports every declared symbol,
+host-side setup (mesh, parameters, ICs) matches the reference's goldens."""
+
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden, golden_meta
+
+
+def _declared_symbols():
+    text = open(os.path.join(ROOT, "include", "uc_b200.h")).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(uc_[a-z_0-9]+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2006_16764_b200 import _lib as L
+
+    lib = L.load()
+    declared = _declared_symbols()
+    assert len(declared) >= 20
+    for name in declared:
+        assert hasattr(lib, name), name
+        assert name in L.SIGNATURES, name
+    assert lib.uc_abi_version() == 1
+
+
+def test_library_is_sm100a():
+    import subprocess
+
+    from paper_2006_16764_b200 import _lib as L
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", L.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_mesh_matches_reference_layout():
+    from paper_2006_16764_b200 import build_mesh
+
+    m = build_mesh(2, (0.48, 0.36), (16, 12))
+    assert m.node_shape == (17, 13) and m.n_nodes == 221 and m.n_elements == 192
+    assert m.spacing == (0.48 / 16, 0.36 / 12)
+    # lexicographic, x fastest; tensor-ordered local nodes (mesh.py:209-228)
+    assert list(m.conn[0]) == [0, 1, 17, 18]
+    assert list(m.conn[16]) == [17, 18, 34, 35]
+    assert np.array_equal(m.coords[17], [0.0, 0.03])
+    m3 = build_mesh(3, (1, 1, 1), (2, 3, 4))
+    assert list(m3.conn[0]) == [0, 1, 3, 4, 12, 13, 15, 16]
+    with pytest.raises(ValueError):
+        build_mesh(4, (1,), (1,))
+
+
+def test_initial_conditions_match_reference():
+    from paper_2006_16764_b200 import AlloyParams, FreeGrowthParams, build_mesh
+    from paper_2006_16764_b200.models import directional_initial_condition, seed_initial_condition
+
+    g = golden("ic")
+    meta = golden_meta()["ic"]
+    m = build_mesh(2, meta["alloy"]["extents"], meta["alloy"]["counts"])
+    ic = directional_initial_condition(m, AlloyParams(), amplitude=0.5, seed=0, smooth=True)
+    assert np.array_equal(ic, g["alloy_256x64"])
+    m2 = build_mesh(2, meta["seed"]["extents"], meta["seed"]["counts"])
+    assert np.array_equal(seed_initial_condition(m2, FreeGrowthParams()), g["seed_128"])
+
+
+def test_device_params_follow_reference_derivations():
+    from paper_2006_16764_b200 import AlloyKernel, FreeGrowthKernel
+    from paper_2006_16764_b200.models import device_params
+
+    fg = device_params(FreeGrowthKernel())
+    assert fg.bg == 191.82 * (1.0 / 191.82)
+    assert fg.tmelt == 1.0 + 0.55 * 1.0
+    assert fg.reg == 1.0
+    al = device_params(AlloyKernel())
+    assert al.dcoef == pytest.approx(6.267, rel=1e-12)
+    assert al.reg == 0.05 ** 4 and al.at_reg2 == 0.02 ** 2
+
+
+def test_unknown_kernel_is_rejected():
+    from paper_2006_16764_b200.models import device_params
+
+    class MassDiffKernel:
+        n_fields = 1
+
+    with pytest.raises(NotImplementedError):
+        device_params(MassDiffKernel())
+
+
+def test_gauss_constants_bitwise_numpy():
+    """The CUDA literals in csrc/uc_common.cuh equal numpy's leggauss(3)."""
+    text = open(os.path.join(ROOT, "paper_2006_16764_b200", "csrc", "uc_common.cuh")).read()
+    lits = dict(re.findall(r"#define (UC_[A-Z0-9]+) (0x[0-9a-fp.+-]+)", text))
+    x, w = np.polynomial.legendre.leggauss(3)
+    assert float.fromhex(lits["UC_GW0"]) == w[0] == w[2]
+    assert float.fromhex(lits["UC_GW1"]) == w[1]
+    assert float.fromhex(lits["UC_LA"]) == (1.0 - x[0]) / 2.0
+    assert float.fromhex(lits["UC_LB"]) == (1.0 + x[0]) / 2.0
+    assert float.fromhex(lits["UC_EPS0"]) == np.sqrt(np.finfo(float).eps)
