@@ -1,0 +1,410 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 hot path (BASELINE.json metric:
+"MDoF/s residual+Jv fill; sec per implicit Newton step at 1/2/4/8 B200").
+
+Default workload = BASELINE.json configs[1]: 2D pure-metal dendrite (free
+growth), Q1 2048x2048 elements on 61.44^2 (h = 0.03), fp64 JFNK.
+
+One timed STEP = one residual fill F(u) plus one fused finite-difference
+Jacobian-vector product J(u)v on the same state (2 x D DoF filled, D = 2 x
+2049^2 = 8,396,802).  ``value`` = whole-job MDoF/s = (sum over ranks of 2 D K)
+/ max-over-ranks time of K steps, inputs resident in HBM (working set ~470 MB,
+larger than the 126 MB L2, so no L2 flush is needed between steps).
+
+Also reported:
+  e2e        the same step through the public API (TimestepResidual.__call__ +
+             jfnk_matvec) with u, v copied from pinned host memory and F, Jv
+             copied back inside the timed region;
+  newton     seconds per implicit Newton iteration for the first (backward-
+             Euler startup) step of the seeded dendrite at the same size, with
+             its GMRES count, preconditioner build and V-cycle apply time;
+  roofline   the residual tile kernel: algorithmic 32 B/DoF (reads u, phi_old,
+             phi_prev, fixed part; writes F) over its CUDA-event duration;
+  cpu_baseline  the oracle port (oracle/uc_oracle.c, OpenMP) on the host cores.
+
+``--impl reference`` times the reference algorithm on the host (the oracle
+port; the reference itself is Python and cannot travel to the GPU box).
+Multi-GPU (torchrun): every rank runs the same per-rank workload (weak scaling,
+independent replicas: the slab-decomposed halo path is not yet wired into
+this benchmark).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: model, dim, extents, counts, theta, dt, step (synthetic states), Newton dt
+    "fg2d_2048": dict(model="free_growth", dim=2, extents=(61.44, 61.44), counts=(2048, 2048),
+                      theta=0.5, dt=2.25e-4, step=2),
+    "fg2d_512": dict(model="free_growth", dim=2, extents=(15.36, 15.36), counts=(512, 512),
+                     theta=0.5, dt=2.25e-4, step=2),
+    "al2d_4096": dict(model="alloy", dim=2, extents=(3276.8, 3276.8), counts=(4096, 4096),
+                      theta=0.5, dt=0.002, step=2),
+    "fg3d_256": dict(model="free_growth", dim=3, extents=(7.68,) * 3, counts=(256,) * 3,
+                     theta=0.5, dt=2.25e-4, step=2),
+}
+
+
+def synthetic_states(w, seed=11):
+    N = int(np.prod([c + 1 for c in w["counts"]]))
+    rng = np.random.default_rng(seed)
+    if w["model"] == "free_growth":  # tests/test_free_growth.py:246-256 distribution
+        mk = lambda: np.concatenate([0.5 + 0.3 * rng.standard_normal(N), 1.0 + 0.2 * rng.standard_normal(N)])  # noqa: E731
+    else:  # tests/test_alloy.py:286-295
+        mk = lambda: np.concatenate([np.tanh(rng.standard_normal(N)), -0.5 + 0.4 * rng.standard_normal(N)])  # noqa: E731
+    u, old, prev = mk(), mk(), mk()
+    v = np.random.default_rng(2).standard_normal(2 * N)
+    return N, u, old, prev, v
+
+
+class Clocks:
+    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def cpu_oracle_step_time(w, steps=2, warmup=1, rows=None):
+    """Residual + Jv of the oracle port on the host; returns (sec/step, D, sample)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+    from paper_2006_16764_b200 import AlloyParams, FreeGrowthParams
+
+    counts = list(w["counts"])
+    extents = list(w["extents"])
+    sample = "full workload"
+    if rows is not None and rows < counts[-1]:
+        # bounded sample: a slab of `rows` element layers of the same mesh
+        extents[-1] = extents[-1] * rows / counts[-1]
+        counts[-1] = rows
+        sample = f"slab of {rows} of {w['counts'][-1]} element layers (same h), scaled per DoF"
+    wl = dict(w, counts=tuple(counts), extents=tuple(extents))
+    N, u, old, prev, v = synthetic_states(wl)
+    params = FreeGrowthParams() if w["model"] == "free_growth" else AlloyParams()
+    p = O.Problem(w["dim"], wl["extents"], wl["counts"], w["model"], params, w["theta"], w["dt"], w["step"])
+    p.begin(old, prev)
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        f = p.residual(u)
+        p.jv(u, f, v)
+        if i >= warmup:
+            times.append(time.perf_counter() - t0)
+    return float(np.mean(times)), 2 * N, sample, O.num_threads()
+
+
+def run_reference(args, w, rank, world):
+    """--impl reference: the reference algorithm on the host (oracle port)."""
+    if rank != 0:
+        return
+    # bounded sample: ~1-2 s per step on a many-core host
+    rows = None if w["dim"] == 2 and np.prod(w["counts"]) <= 2048 * 2048 else 256
+    sec, D, sample, cores = cpu_oracle_step_time(w, steps=args.steps, warmup=args.warmup, rows=rows)
+    mdofs = 2 * D / sec / 1e6
+    line = {
+        "impl": "reference", "metric": "MDoF/s residual+Jv fill", "value": round(mdofs, 4),
+        "unit": "MDoF/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, **{k: w[k] for k in ("model", "dim", "counts")}},
+        "cpu_baseline": {"value": round(mdofs, 4), "unit": "MDoF/s", "cores": cores, "kind": "port",
+                         "sample": sample},
+        "e2e": {"value": round(mdofs, 4), "unit": "MDoF/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def vcycle_bytes(pc, N, dim):
+    """Algorithmic HBM bytes of one BlockPrecond.apply (both blocks), counting
+    stencil + vector streams once per pass (x neighbours cached)."""
+    K = 3 ** dim
+    cfg = pc.cfg
+    rows = [int(np.prod(s)) for s in pc.level_shapes]
+    sweep = lambda R: (8 * K + 24) * R  # noqa: E731  one half-sweep: A rows, b, x r/w
+    total = 0.0
+
+    def cyc(l):
+        nonlocal total
+        R = rows[l]
+        total += 8 * R  # zero x
+        if l == len(rows) - 1:
+            total += 2 * cfg.coarse_sweeps * sweep(R)
+            return
+        total += 4 * cfg.sweeps * sweep(R) / 2 * 2  # pre + post, forward + reverse
+        total += (8 * K + 24) * R  # residual
+        total += 8 * R + 8 * rows[l + 1]  # restrict
+        cyc(l + 1)
+        total += 8 * rows[l + 1] + 16 * R  # prolong-add
+
+    for c in range(cfg.cycles):
+        cyc(0)
+        if c > 0:
+            total += (8 * K + 24) * rows[0] + 24 * rows[0]  # residual + x += e
+    return 2 * total  # both field blocks
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="fg2d_2048", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-newton", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    w = WORKLOADS[args.workload]
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, w, rank, world)
+        return
+
+    import torch
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    import paper_2006_16764_b200 as uc
+    from paper_2006_16764_b200 import device as D
+    from paper_2006_16764_b200.models import seed_initial_condition
+
+    dev = torch.device("cuda", local)
+    N, u_h, old_h, prev_h, v_h = synthetic_states(w)
+    Dof = 2 * N
+    mesh = uc.build_mesh(w["dim"], w["extents"], w["counts"])
+    kern = uc.FreeGrowthKernel() if w["model"] == "free_growth" else uc.AlloyKernel()
+    sc = uc.ThetaScheme(w["theta"], w["dt"], w["step"])
+    u = torch.from_numpy(u_h).to(dev)
+    v = torch.from_numpy(v_h).to(dev)
+    res = uc.TimestepResidual(mesh, kern, torch.from_numpy(old_h).to(dev),
+                              torch.from_numpy(prev_h).to(dev), sc)
+    unorm = D.norm(u)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        f = res.device_call(u, check=False)
+        return res.jv_device(u, f, v, unorm)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- device-resident throughput ------------------------------------
+    clk = Clocks(local).__enter__()  # sampled from warm-up through the kernel timings
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
+    value = world * 2 * Dof / (ms * 1e-3) / 1e6
+    if res.ctx.status().residual_nonfinite:
+        raise RuntimeError("non-finite residual in benchmark inputs")
+
+    # ---- per-kernel durations (CUDA events on the launching stream) ----
+    def timed(fn, reps):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    f0 = res.device_call(u, check=False)
+    t_res = timed(lambda: res.device_call(u, check=False), max(args.steps, 50))
+    t_jv = timed(lambda: res.jv_device(u, f0, v, unorm), max(args.steps, 50))
+    clk.__exit__()
+    peaks = {}
+    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pk):
+        with open(pk) as fh:
+            peaks = json.load(fh)
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    res_bytes = 32 * Dof
+    achieved = res_bytes / (t_res * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                "kernel": f"k_residual<{w['dim']},{'FG' if w['model'] == 'free_growth' else 'ALLOY'},NEW>",
+                "bytes_per_dof": 32, "ms_per_launch": round(t_res, 4), "peak_source": peak_src,
+                "note": "fp64-issue-bound kernel; HBM fraction ceiling ~20-30% in 2D (DESIGN.md)"}
+    kernels = {"residual_ms": round(t_res, 4), "jv_ms": round(t_jv, 4),
+               "residual_mdofs": round(Dof / (t_res * 1e-3) / 1e6, 1),
+               "jv_mdofs": round(Dof / (t_jv * 1e-3) / 1e6, 1),
+               "jv_gbs": round(48 * Dof / (t_jv * 1e-3) / 1e9, 1)}
+
+    # ---- end-to-end through the public API with host buffers ----------
+    u_pin = torch.from_numpy(u_h).pin_memory()
+    v_pin = torch.from_numpy(v_h).pin_memory()
+    f_pin = torch.empty(Dof, dtype=torch.float64).pin_memory()
+    j_pin = torch.empty(Dof, dtype=torch.float64).pin_memory()
+    u_d = torch.empty(Dof, dtype=torch.float64, device=dev)
+    v_d = torch.empty(Dof, dtype=torch.float64, device=dev)
+
+    def e2e_step():
+        u_d.copy_(u_pin, non_blocking=True)
+        v_d.copy_(v_pin, non_blocking=True)
+        F = res(u_d)
+        Jv = uc.jfnk_matvec(res, u_d, F, v_d)
+        f_pin.copy_(F, non_blocking=True)
+        j_pin.copy_(Jv, non_blocking=True)
+
+    for _ in range(args.warmup):
+        e2e_step()
+    barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(args.steps):
+        e2e_step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = max_over_ranks(a.elapsed_time(b) / args.steps)
+    e2e = {"value": round(world * 2 * Dof / (e2e_ms * 1e-3) / 1e6, 2), "unit": "MDoF/s",
+           "h2d_bytes_per_step": 2 * Dof * 8, "d2h_bytes_per_step": 2 * Dof * 8,
+           "ms_per_step": round(e2e_ms, 3)}
+    launches_per_step = 3  # residual tile, |v| reduction, Jv tile
+
+    # ---- Newton step on the seeded dendrite --------------------------
+    newton = None
+    if not args.no_newton and w["model"] == "free_growth":
+        u0 = seed_initial_condition(mesh, kern.params) if w["dim"] == 2 or N < 5e7 else None
+        if u0 is not None:
+            st = torch.from_numpy(u0).to(dev)
+            sc0 = uc.ThetaScheme(1.0, w["dt"], 0)
+            walls = []
+            for rep_i in range(2):  # cold (first) and warm (allocator/JIT warm) solves
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                pc = uc.build_precond(mesh, kern, st, sc0, uc.PrecondConfig(ordering="multicolor"))
+                torch.cuda.synchronize()
+                t_build = time.perf_counter() - t0
+                r0 = uc.TimestepResidual(mesh, kern, st, st, sc0)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                _, rep = uc.newton_solve(r0, st, uc.NewtonConfig(), precond_apply=pc.apply)
+                torch.cuda.synchronize()
+                walls.append(time.perf_counter() - t0)
+            t_newton = walls[-1]
+            t_apply = timed(lambda: pc.device_apply(v, check=False), 5)
+            vb = vcycle_bytes(pc, N, w["dim"])
+            newton = {"sec_per_newton_iteration": round(t_newton / max(rep.iterations, 1), 5),
+                      "newton_iterations": rep.iterations, "gmres_per_newton": rep.gmres_iterations,
+                      "converged": bool(rep.converged), "precond_build_s": round(t_build, 4),
+                      "cold_sec_per_newton_iteration": round(walls[0] / max(rep.iterations, 1), 5),
+                      "vcycle_apply_ms": round(t_apply, 3),
+                      "vcycle_gbs": round(vb / (t_apply * 1e-3) / 1e9, 1),
+                      "vcycle_hbm_frac": round(vb / (t_apply * 1e-3) / 1e9 / hbm_peak, 4),
+                      "case": "seed IC, step 0 (backward-Euler startup), default solver settings"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            sec, Dc, sample, cores = cpu_oracle_step_time(w, steps=1, warmup=1,
+                                                         rows=None if w["dim"] == 2 and N <= 2049 ** 2 else 128)
+            cpu = {"value": round(2 * Dc / sec / 1e6, 4), "unit": "MDoF/s", "cores": cores,
+                   "kind": "port", "sample": sample + "; residual+Jv of oracle/uc_oracle.c (OpenMP)"}
+        except Exception as exc:  # reported, not fatal
+            cpu = {"value": None, "unit": "MDoF/s", "cores": 0, "kind": "port", "sample": f"failed: {exc}"}
+
+    if rank == 0:
+        line = {
+            "metric": "MDoF/s residual+Jv fill", "value": round(value, 2), "unit": "MDoF/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.workload, "model": w["model"], "dim": w["dim"],
+                       "counts": list(w["counts"]), "dof": Dof, "dof_per_step": 2 * Dof,
+                       "l2": "inputs (~470 MB working set) larger than L2; no flush",
+                       "parallelism": f"replicas x{world}"},
+            "roofline": roofline, "kernels": kernels, "e2e": e2e,
+            "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(),
+            "newton": newton, "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()
