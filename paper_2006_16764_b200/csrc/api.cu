@@ -87,8 +87,13 @@ int uc_ctx_create(const uc_mesh_desc* mesh, const uc_model_params* params, void*
   if (e == cudaSuccess) e = cudaMalloc(&c->scal, sizeof(double) * UC_SCAL_SLOTS);
   if (e == cudaSuccess) e = cudaMemset(c->scal, 0, sizeof(double) * UC_SCAL_SLOTS);
   if (e == cudaSuccess) e = cudaMallocHost(&c->pinned, sizeof(double) * UC_SCAL_SLOTS);
-  if (e == cudaSuccess) e = cudaMalloc(&c->flags, sizeof(unsigned int) * 4);
-  if (e == cudaSuccess) e = cudaMemset(c->flags, 0, sizeof(unsigned int) * 4);
+  // status flags live in mapped pinned host memory: kernels set them, the
+  // host reads them after a stream sync without a device->host copy
+  if (e == cudaSuccess) e = cudaHostAlloc(&c->flags_host, sizeof(unsigned int) * 4, cudaHostAllocMapped);
+  if (e == cudaSuccess) {
+    memset(c->flags_host, 0, sizeof(unsigned int) * 4);
+    e = cudaHostGetDevicePointer(&c->flags, c->flags_host, 0);
+  }
   if (e == cudaSuccess) e = cudaMalloc(&c->locate_key, sizeof(unsigned long long));
   const Grid& g = c->grid;
   if (e == cudaSuccess && g.lo > 0) {
@@ -113,7 +118,7 @@ int uc_ctx_destroy(uc_ctx* c) {
   cudaFree(c->ticket);
   cudaFree(c->scal);
   if (c->pinned) cudaFreeHost(c->pinned);
-  cudaFree(c->flags);
+  if (c->flags_host) cudaFreeHost(c->flags_host);
   cudaFree(c->locate_key);
   for (int s = 0; s < 4; ++s)
     for (int d = 0; d < 2; ++d) cudaFree(c->ghost[s][d]);
@@ -177,14 +182,17 @@ int uc_jv(uc_ctx* c, const uc_scheme* sc, const double* u, const double* fu, con
 
 int uc_status(uc_ctx* c, uc_status_t* out, int clear) {
   if (!c || !out) return set_error(UC_ERR_ARG, "uc_status: NULL argument");
-  unsigned int f[4];
-  UC_CUDA_OK(cudaMemcpyAsync(f, c->flags, sizeof(f), cudaMemcpyDeviceToHost, c->stream));
   UC_CUDA_OK(cudaStreamSynchronize(c->stream));
+  volatile unsigned int* f = c->flags_host;
   out->residual_nonfinite = (int)f[0];
   out->precond_nonfinite = (int)f[1];
   out->precond_bad_diag = (int)f[2];
   out->pad = 0;
-  if (clear) UC_CUDA_OK(cudaMemsetAsync(c->flags, 0, sizeof(f), c->stream));
+  if (clear) {
+    f[0] = 0u;
+    f[1] = 0u;
+    f[2] = 0u;
+  }
   return UC_OK;
 }
 

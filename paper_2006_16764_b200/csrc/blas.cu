@@ -150,7 +150,7 @@ __global__ void k_nonfinite(int64_t n, const double* __restrict__ a, unsigned in
   bool bad = false;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
     bad |= !isfinite(a[i]);
-  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *(volatile unsigned int*)flag = 1u;
 }
 
 static inline unsigned ew_grid(uc_ctx* c, int64_t n) {
@@ -168,7 +168,14 @@ int launch_axpy(uc_ctx* c, int64_t n, const double* a, double s, const double* b
 }
 
 int nonfinite_flag(uc_ctx* c, int64_t n, const double* a, unsigned int* flag) {
-  k_nonfinite<<<ew_grid(c, n), 256, 0, c->stream>>>(n, a, flag);
+  return nonfinite_flag_on(c->stream, n, a, flag);
+}
+
+int nonfinite_flag_on(cudaStream_t s, int64_t n, const double* a, unsigned int* flag) {
+  int64_t b = (n + 255) / 256;
+  if (b > 148 * 16) b = 148 * 16;
+  if (b < 1) b = 1;
+  k_nonfinite<<<(unsigned)b, 256, 0, s>>>(n, a, flag);
   UC_CUDA_OK(cudaGetLastError());
   return UC_OK;
 }

@@ -49,6 +49,25 @@ struct Grid {
   double ih[3];    // 1/h as the reference's 0.5*(2/h)
 };
 
+// Division by a run-time constant via multiply-high (CUTLASS FastDivmod
+// scheme): n / d == umulhi(n, m) >> s for 0 <= n < 2^31.
+struct FastDiv {
+  uint32_t d, m, s;
+  static FastDiv make(uint32_t d) {
+    FastDiv f{d, 0u, 0u};
+    if (d <= 1) return f;
+    uint32_t l = 0;
+    while ((1ull << l) < d) ++l;
+    const uint64_t p = 31 + l;
+    f.m = (uint32_t)(((1ull << p) + d - 1) / d);
+    f.s = (uint32_t)(p - 32);
+    return f;
+  }
+  __device__ __forceinline__ uint32_t div(uint32_t n) const {
+    return d <= 1 ? n : (__umulhi(n, m) >> s);
+  }
+};
+
 // Field view: owned block-ordered array plus optional ghost planes.
 struct FieldView {
   const double* owned;   // [2][nloc]

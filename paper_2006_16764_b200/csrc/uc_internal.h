@@ -46,7 +46,8 @@ struct uc_ctx {
   unsigned int* ticket = nullptr;
   double* scal = nullptr;        // [UC_SCAL_SLOTS] device scalars
   double* pinned = nullptr;      // [UC_SCAL_SLOTS] pinned host staging
-  unsigned int* flags = nullptr; // [4] sticky status flags
+  unsigned int* flags = nullptr;      // [4] sticky status flags (device alias)
+  unsigned int* flags_host = nullptr; // mapped pinned host memory
   unsigned long long* locate_key = nullptr;
   // ghost planes [slot][side] -> [2][plane]
   double* ghost[4][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
@@ -58,6 +59,7 @@ namespace uc {
 int reduce_dot(uc_ctx* c, int64_t n, const double* a, const double* b, double* out_dev,
                bool sqrt_result);
 int nonfinite_flag(uc_ctx* c, int64_t n, const double* a, unsigned int* flag);
+int nonfinite_flag_on(cudaStream_t s, int64_t n, const double* a, unsigned int* flag);
 int launch_axpy(uc_ctx* c, int64_t n, const double* a, double s, const double* b, double* out);
 // residual.cu
 enum { MODE_NEW = 0, MODE_OLD = 1, MODE_JV = 2 };

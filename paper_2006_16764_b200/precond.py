@@ -130,6 +130,15 @@ class BlockPrecond:
             raise FloatingPointError("preconditioner produced non-finite values")
         return out
 
+    # deferred-check protocol used by gmres_solve: launch without a sync, then
+    # check the sticky flag once the caller has synchronised anyway
+    def _uc_deferred(self, v: torch.Tensor) -> torch.Tensor:
+        return self.device_apply(v, check=False)
+
+    def _uc_check(self) -> None:
+        if self._ctx.status(clear=True).precond_nonfinite:
+            raise FloatingPointError("preconditioner produced non-finite values")
+
     def apply(self, v):
         if D.is_device(v):
             return self.device_apply(D.as_device(v))
