@@ -201,6 +201,41 @@ int uc_precond_levels(uc_ctx* ctx, int64_t* shapes /* [levels][3] */);
 /* Sticky status flags (synchronises); clear=1 resets them. */
 int uc_status(uc_ctx* ctx, uc_status_t* out, int clear);
 
+/* ---- Slab decomposition (paper §4 MPI subdomains) --------
+ * Every *_group entry point takes the slabs driven by this process, ordered
+ * by their slab_lo, with block vectors of the owned planes per slab.  Slab
+ * neighbours are either local contexts (uc_ctx_link_local: same process and
+ * device, planes copied on the stream — single-GPU emulation of k ranks) or
+ * remote NCCL ranks (uc_comm_init_nccl + uc_ctx_set_neighbors: one process
+ * per GPU, ncclSend/ncclRecv of one plane per field block, ncclAllReduce of
+ * every dot product).  The single-context entry points above are the n = 1
+ * case and are distributed automatically once a context has remote
+ * neighbours. */
+int uc_nccl_unique_id(const char* nccl_path, void* out128);
+int uc_comm_init_nccl(const char* nccl_path, const void* id128, int rank, int nranks);
+int uc_comm_finalize(void);
+int uc_ctx_set_neighbors(uc_ctx* ctx, int lo_rank, int hi_rank);
+int uc_ctx_link_local(uc_ctx* lower, uc_ctx* upper);
+
+int uc_residual_group(uc_ctx* const* ctxs, int n, const uc_scheme* sc, int part,
+                      const double* const* unew, const double* const* old,
+                      const double* const* prev, const double* const* fixed,
+                      double* const* out);
+int uc_jv_group(uc_ctx* const* ctxs, int n, const uc_scheme* sc, const double* const* u,
+                const double* const* fu, const double* const* v, double unorm,
+                const double* const* old, const double* const* prev,
+                const double* const* fixed, double* const* jv, double* eps_out);
+/* global dot (b != NULL) or norm (b == NULL, do_sqrt = 1) over all slabs; synchronises */
+int uc_dot_group(uc_ctx* const* ctxs, int n, const double* const* a, const double* const* b,
+                 int do_sqrt, double* out);
+/* basis: n x (k+2) device pointers (row per slab, slot k+1 is the output) */
+int uc_arnoldi_group(uc_ctx* const* ctxs, int n, const double* const* basis, int k,
+                     double* const* w, double scale, double* h_host, int* broke);
+int uc_precond_build_group(uc_ctx* const* ctxs, int n, const uc_scheme* sc,
+                           const double* const* states, const uc_precond_cfg* cfg);
+int uc_precond_apply_group(uc_ctx* const* ctxs, int n, const double* const* v,
+                           double* const* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -79,6 +79,21 @@ SIGNATURES = {
     "uc_precond_stencil": (_I, [_P, _I, _I, _P]),
     "uc_precond_levels": (_I, [_P, C.POINTER(_I64)]),
     "uc_status": (_I, [_P, C.POINTER(Status), _I]),
+    "uc_nccl_unique_id": (_I, [C.c_char_p, _P]),
+    "uc_comm_init_nccl": (_I, [C.c_char_p, _P, _I, _I]),
+    "uc_comm_finalize": (_I, []),
+    "uc_ctx_set_neighbors": (_I, [_P, _I, _I]),
+    "uc_ctx_link_local": (_I, [_P, _P]),
+    "uc_residual_group": (_I, [C.POINTER(_P), _I, C.POINTER(Scheme), _I] + [C.POINTER(_P)] * 5),
+    "uc_jv_group": (_I, [C.POINTER(_P), _I, C.POINTER(Scheme), C.POINTER(_P), C.POINTER(_P),
+                         C.POINTER(_P), _D, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P),
+                         C.POINTER(_P), _P]),
+    "uc_dot_group": (_I, [C.POINTER(_P), _I, C.POINTER(_P), C.POINTER(_P), _I, C.POINTER(_D)]),
+    "uc_arnoldi_group": (_I, [C.POINTER(_P), _I, C.POINTER(_P), _I, C.POINTER(_P), _D,
+                              C.POINTER(_D), C.POINTER(_I)]),
+    "uc_precond_build_group": (_I, [C.POINTER(_P), _I, C.POINTER(Scheme), C.POINTER(_P),
+                                    C.POINTER(PrecondCfg)]),
+    "uc_precond_apply_group": (_I, [C.POINTER(_P), _I, C.POINTER(_P), C.POINTER(_P)]),
 }
 
 _lock = threading.Lock()
@@ -115,3 +130,8 @@ def check(rc: int, what: str = "") -> None:
 
 def ptr(t) -> C.c_void_p:
     return C.c_void_p(t.data_ptr())
+
+
+def ptrs(ts) -> "C.Array":
+    """ctypes void* array of tensor data pointers (None allowed)."""
+    return (C.c_void_p * len(ts))(*[None if t is None else t.data_ptr() for t in ts])

@@ -97,10 +97,10 @@ int uc_ctx_create(const uc_mesh_desc* mesh, const uc_model_params* params, void*
   if (e == cudaSuccess) e = cudaMalloc(&c->locate_key, sizeof(unsigned long long));
   const Grid& g = c->grid;
   if (e == cudaSuccess && g.lo > 0) {
-    for (int s = 0; s < 4 && e == cudaSuccess; ++s) e = cudaMalloc(&c->ghost[s][0], sizeof(double) * 2 * g.plane);
+    for (int s = 0; s < 5 && e == cudaSuccess; ++s) e = cudaMalloc(&c->ghost[s][0], sizeof(double) * 2 * g.plane);
   }
   if (e == cudaSuccess && g.hi < g.nslow) {
-    for (int s = 0; s < 4 && e == cudaSuccess; ++s) e = cudaMalloc(&c->ghost[s][1], sizeof(double) * 2 * g.plane);
+    for (int s = 0; s < 5 && e == cudaSuccess; ++s) e = cudaMalloc(&c->ghost[s][1], sizeof(double) * 2 * g.plane);
   }
   if (e != cudaSuccess) {
     rc = set_cuda_error(e, "uc_ctx_create allocation", __FILE__, __LINE__);
@@ -120,7 +120,7 @@ int uc_ctx_destroy(uc_ctx* c) {
   if (c->pinned) cudaFreeHost(c->pinned);
   if (c->flags_host) cudaFreeHost(c->flags_host);
   cudaFree(c->locate_key);
-  for (int s = 0; s < 4; ++s)
+  for (int s = 0; s < 5; ++s)
     for (int d = 0; d < 2; ++d) cudaFree(c->ghost[s][d]);
   delete c;
   return UC_OK;
@@ -135,21 +135,40 @@ int uc_set_stream(uc_ctx* c, void* stream) {
 int64_t uc_n_local(const uc_ctx* c) { return c ? c->grid.nloc : -1; }
 
 double* uc_ghost_ptr(uc_ctx* c, int slot, int side) {
-  if (!c || slot < 0 || slot > 3 || side < 0 || side > 1) return nullptr;
+  if (!c || slot < 0 || slot > 4 || side < 0 || side > 1) return nullptr;
   return c->ghost[slot][side];
+}
+
+int uc_residual_group(uc_ctx* const* ctxs, int n, const uc_scheme* sc, int part,
+                      const double* const* unew, const double* const* old,
+                      const double* const* prev, const double* const* fixed, double* const* out) {
+  if (!ctxs || n < 1 || !sc || !old || !prev || !out)
+    return set_error(UC_ERR_ARG, "uc_residual: NULL argument");
+  if (!(sc->dt > 0.0) || sc->theta < 0.0 || sc->theta > 1.0)
+    return set_error(UC_ERR_ARG, "uc_residual: bad scheme");
+  if (part != UC_PART_OLD && (part != UC_PART_NEW || !unew || !fixed))
+    return set_error(UC_ERR_ARG, "uc_residual: bad part");
+  Group G(ctxs, ctxs + n);
+  cudaStream_t s = G[0]->stream;
+  int rc;
+  if ((rc = halo_vectors(G, 1, old, s))) return rc;
+  if ((rc = halo_vectors(G, 2, prev, s))) return rc;
+  if (part == UC_PART_NEW && (rc = halo_vectors(G, 0, unew, s))) return rc;
+  for (int i = 0; i < n; ++i) {
+    if (part == UC_PART_OLD)
+      rc = launch_residual(G[i], sc, MODE_OLD, nullptr, old[i], prev[i], nullptr, nullptr, nullptr,
+                           out[i], 0.0, nullptr, nullptr);
+    else
+      rc = launch_residual(G[i], sc, MODE_NEW, unew[i], old[i], prev[i], nullptr, nullptr, fixed[i],
+                           out[i], 0.0, nullptr, nullptr);
+    if (rc) return rc;
+  }
+  return UC_OK;
 }
 
 int uc_residual(uc_ctx* c, const uc_scheme* sc, int part, const double* unew, const double* old,
                 const double* prev, const double* fixed, double* out) {
-  if (!c || !sc || !old || !prev || !out) return set_error(UC_ERR_ARG, "uc_residual: NULL argument");
-  if (!(sc->dt > 0.0) || sc->theta < 0.0 || sc->theta > 1.0)
-    return set_error(UC_ERR_ARG, "uc_residual: bad scheme");
-  if (part == UC_PART_OLD)
-    return launch_residual(c, sc, MODE_OLD, nullptr, old, prev, nullptr, nullptr, nullptr, out,
-                           0.0, nullptr, nullptr);
-  if (part != UC_PART_NEW || !unew || !fixed) return set_error(UC_ERR_ARG, "uc_residual: bad part");
-  return launch_residual(c, sc, MODE_NEW, unew, old, prev, nullptr, nullptr, fixed, out, 0.0,
-                         nullptr, nullptr);
+  return uc_residual_group(&c, 1, sc, part, &unew, &old, &prev, &fixed, &out);
 }
 
 int uc_locate_nonfinite(uc_ctx* c, const uc_scheme* sc, int part, const double* unew,
@@ -167,17 +186,70 @@ int uc_locate_nonfinite(uc_ctx* c, const uc_scheme* sc, int part, const double* 
   return UC_OK;
 }
 
+int uc_jv_group(uc_ctx* const* ctxs, int n, const uc_scheme* sc, const double* const* u,
+                const double* const* fu, const double* const* v, double unorm,
+                const double* const* old, const double* const* prev, const double* const* fixed,
+                double* const* jv, double* eps_out) {
+  if (!ctxs || n < 1 || !sc || !u || !fu || !v || !old || !prev || !fixed || !jv)
+    return set_error(UC_ERR_ARG, "uc_jv: NULL argument");
+  Group G(ctxs, ctxs + n);
+  cudaStream_t s = G[0]->stream;
+  int rc;
+  if ((rc = halo_vectors(G, 1, old, s))) return rc;
+  if ((rc = halo_vectors(G, 2, prev, s))) return rc;
+  if ((rc = halo_vectors(G, 0, u, s))) return rc;
+  if ((rc = halo_vectors(G, 3, v, s))) return rc;
+  // |v| on the device (newton.py:108), then eps = EPS0*sqrt(1+|u|)/|v| in-kernel
+  std::vector<double*> vn(n);
+  const bool sum = group_needs_sum(G);
+  for (int i = 0; i < n; ++i) {
+    vn[i] = G[i]->scal + (UC_SCAL_SLOTS - 1);
+    if ((rc = reduce_dot(G[i], 2 * G[i]->grid.nloc, v[i], nullptr, vn[i], !sum))) return rc;
+  }
+  if (sum && (rc = global_sum(G, vn.data(), true, s))) return rc;
+  const double eps_num = UC_EPS0 * sqrt(1.0 + unorm);
+  for (int i = 0; i < n; ++i)
+    if ((rc = launch_residual(G[i], sc, MODE_JV, u[i], old[i], prev[i], v[i], fu[i], fixed[i], jv[i],
+                              eps_num, vn[i], i == 0 ? eps_out : nullptr)))
+      return rc;
+  return UC_OK;
+}
+
 int uc_jv(uc_ctx* c, const uc_scheme* sc, const double* u, const double* fu, const double* v,
           double unorm, const double* old, const double* prev, const double* fixed, double* jv,
           double* eps_out) {
-  if (!c || !sc || !u || !fu || !v || !old || !prev || !fixed || !jv)
-    return set_error(UC_ERR_ARG, "uc_jv: NULL argument");
-  // |v| on the device (newton.py:108), then eps = EPS0*sqrt(1+|u|)/|v| in-kernel
-  double* vnorm = c->scal + (UC_SCAL_SLOTS - 1);
-  int rc = reduce_dot(c, 2 * c->grid.nloc, v, nullptr, vnorm, true);
-  if (rc) return rc;
-  const double eps_num = UC_EPS0 * sqrt(1.0 + unorm);
-  return launch_residual(c, sc, MODE_JV, u, old, prev, v, fu, fixed, jv, eps_num, vnorm, eps_out);
+  return uc_jv_group(&c, 1, sc, &u, &fu, &v, unorm, &old, &prev, &fixed, &jv, eps_out);
+}
+
+int uc_dot_group(uc_ctx* const* ctxs, int n, const double* const* a, const double* const* b,
+                 int do_sqrt, double* out) {
+  if (!ctxs || n < 1 || !a || !out) return set_error(UC_ERR_ARG, "uc_dot_group: NULL argument");
+  Group G(ctxs, ctxs + n);
+  cudaStream_t s = G[0]->stream;
+  std::vector<double*> slot(n);
+  int rc;
+  for (int i = 0; i < n; ++i) {
+    slot[i] = G[i]->scal + (UC_SCAL_SLOTS - 2);
+    if ((rc = reduce_dot(G[i], 2 * G[i]->grid.nloc, a[i], b ? b[i] : nullptr, slot[i], false))) return rc;
+  }
+  if ((rc = global_sum(G, slot.data(), do_sqrt != 0, s))) return rc;
+  UC_CUDA_OK(cudaMemcpyAsync(G[0]->pinned, slot[0], sizeof(double), cudaMemcpyDeviceToHost, s));
+  UC_CUDA_OK(cudaStreamSynchronize(s));
+  *out = G[0]->pinned[0];
+  return UC_OK;
+}
+
+int uc_precond_build_group(uc_ctx* const* ctxs, int n, const uc_scheme* sc,
+                           const double* const* states, const uc_precond_cfg* cfg) {
+  if (!ctxs || n < 1 || !sc || !states || !cfg) return set_error(UC_ERR_ARG, "uc_precond_build: NULL argument");
+  Group G(ctxs, ctxs + n);
+  return precond_build_group(G, sc, states, cfg);
+}
+
+int uc_precond_apply_group(uc_ctx* const* ctxs, int n, const double* const* v, double* const* out) {
+  if (!ctxs || n < 1 || !v || !out) return set_error(UC_ERR_ARG, "uc_precond_apply: NULL argument");
+  Group G(ctxs, ctxs + n);
+  return precond_apply_group(G, v, out);
 }
 
 int uc_status(uc_ctx* c, uc_status_t* out, int clear) {

@@ -192,7 +192,10 @@ int uc_dot(uc_ctx* c, int64_t n, const double* a, const double* b, double* out_d
     UC_CUDA_OK(cudaMemsetAsync(out_dev, 0, sizeof(double), c->stream));
     return UC_OK;
   }
-  return reduce_dot(c, n, a, b, out_dev, false);
+  int rc = reduce_dot(c, n, a, b, out_dev, false);
+  if (rc || !c->dist) return rc;
+  Group G{c};
+  return global_sum(G, &out_dev, false, c->stream);
 }
 
 int uc_norm(uc_ctx* c, int64_t n, const double* a, double* out_dev) {
@@ -201,7 +204,11 @@ int uc_norm(uc_ctx* c, int64_t n, const double* a, double* out_dev) {
     UC_CUDA_OK(cudaMemsetAsync(out_dev, 0, sizeof(double), c->stream));
     return UC_OK;
   }
-  return reduce_dot(c, n, a, nullptr, out_dev, true);
+  if (!c->dist) return reduce_dot(c, n, a, nullptr, out_dev, true);
+  int rc = reduce_dot(c, n, a, nullptr, out_dev, false);
+  if (rc) return rc;
+  Group G{c};
+  return global_sum(G, &out_dev, true, c->stream);
 }
 
 int uc_dot_host(uc_ctx* c, int64_t n, const double* a, const double* b, double* out) {
@@ -222,36 +229,74 @@ int uc_norm_host(uc_ctx* c, int64_t n, const double* a, double* out) {
   return UC_OK;
 }
 
-int uc_arnoldi(uc_ctx* c, int64_t n, const double* const* basis, int k, double* w, double scale,
-               double* h_host, int* broke) {
-  if (!c || !basis || !w || k < 0 || 3 * (k + 2) + 8 > UC_SCAL_SLOTS)
-    return set_error(UC_ERR_ARG, "uc_arnoldi: bad argument (k=%d)", k);
-  // scalar layout: [0, k+2) h; then 2(k+1)+1 dot slots
-  double* h = c->scal;
-  double* slots = c->scal + (k + 2);
+// MGS over a group of slabs: per-projection global sums between the fused
+// projection kernels (no host round trip); one D2H of h at the end.
+static int arnoldi_group(const Group& G, const int64_t* n, const double* const* const* basis, int k,
+                         double* const* w, double scale, double* h_host, int* broke) {
+  const int ns = (int)G.size();
+  if (k < 0 || 3 * (k + 2) + 8 > UC_SCAL_SLOTS) return set_error(UC_ERR_ARG, "uc_arnoldi: bad k=%d", k);
+  cudaStream_t s = G[0]->stream;
+  const bool sum = group_needs_sum(G);
+  // per slab scalar layout: [0, k+2) h; then 2(k+1)+1 dot slots
+  std::vector<double*> slot(ns);
+  int rc;
+  for (int i = 0; i < ns; ++i) {
+    slot[i] = G[i]->scal + (k + 2);
+    if ((rc = reduce_dot(G[i], n[i], basis[i][0], w[i], slot[i], false))) return rc;
+  }
+  if (sum && (rc = global_sum(G, slot.data(), false, s))) return rc;
   const int m = 2 * (k + 1);
-  int rc = reduce_dot(c, n, basis[0], w, &slots[0], false);
-  if (rc) return rc;
-  const unsigned grid = red_grid(n);
   for (int t = 0; t < m; ++t) {
     const int j = t % (k + 1);
     const bool last = (t + 1 == m);
-    const double* vnext = last ? nullptr : basis[(t + 1) % (k + 1)];
-    k_mgs<<<grid, UC_RED_THREADS, 0, c->stream>>>(n, basis[j], w, vnext, &slots[t], &h[j],
-                                                  t >= k + 1 ? 1 : 0, c->partials, c->ticket,
-                                                  last ? &h[k + 1] : &slots[t + 1], last ? 1 : 0);
-    UC_CUDA_OK(cudaGetLastError());
+    for (int i = 0; i < ns; ++i) {
+      uc_ctx* c = G[i];
+      double* h = c->scal;
+      double* sl = c->scal + (k + 2);
+      const double* vnext = last ? nullptr : basis[i][(t + 1) % (k + 1)];
+      k_mgs<<<red_grid(n[i]), UC_RED_THREADS, 0, s>>>(n[i], basis[i][j], w[i], vnext, &sl[t], &h[j],
+                                                      t >= k + 1 ? 1 : 0, c->partials, c->ticket,
+                                                      last ? &h[k + 1] : &sl[t + 1], (last && !sum) ? 1 : 0);
+      UC_CUDA_OK(cudaGetLastError());
+    }
+    if (sum) {
+      std::vector<double*> nx(ns);
+      for (int i = 0; i < ns; ++i) nx[i] = last ? &G[i]->scal[k + 1] : G[i]->scal + (k + 2) + t + 1;
+      if ((rc = global_sum(G, nx.data(), last, s))) return rc;
+    }
   }
   const double tol = 1e-14 * scale;  // BREAKDOWN_TOL * scale (krylov.py:13,67)
-  k_normalize<<<ew_grid(c, n), 256, 0, c->stream>>>(n, w, &h[k + 1], tol,
-                                                    const_cast<double*>(basis[k + 1]));
-  UC_CUDA_OK(cudaGetLastError());
-  UC_CUDA_OK(cudaMemcpyAsync(c->pinned, h, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost,
-                             c->stream));
-  UC_CUDA_OK(cudaStreamSynchronize(c->stream));
-  for (int i = 0; i < k + 2; ++i) h_host[i] = c->pinned[i];
+  for (int i = 0; i < ns; ++i) {
+    k_normalize<<<ew_grid(G[i], n[i]), 256, 0, s>>>(n[i], w[i], &G[i]->scal[k + 1], tol,
+                                                    const_cast<double*>(basis[i][k + 1]));
+    UC_CUDA_OK(cudaGetLastError());
+  }
+  UC_CUDA_OK(cudaMemcpyAsync(G[0]->pinned, G[0]->scal, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost, s));
+  UC_CUDA_OK(cudaStreamSynchronize(s));
+  for (int i = 0; i < k + 2; ++i) h_host[i] = G[0]->pinned[i];
   *broke = (h_host[k + 1] < tol) ? 1 : 0;
   return UC_OK;
+}
+
+int uc_arnoldi(uc_ctx* c, int64_t n, const double* const* basis, int k, double* w, double scale,
+               double* h_host, int* broke) {
+  if (!c || !basis || !w) return set_error(UC_ERR_ARG, "uc_arnoldi: bad argument");
+  Group G{c};
+  return arnoldi_group(G, &n, &basis, k, &w, scale, h_host, broke);
+}
+
+// basis: n slabs x (k+2) device pointers, row-major
+int uc_arnoldi_group(uc_ctx* const* ctxs, int nslabs, const double* const* basis, int k,
+                     double* const* w, double scale, double* h_host, int* broke) {
+  if (!ctxs || nslabs < 1 || !basis || !w) return set_error(UC_ERR_ARG, "uc_arnoldi_group: bad argument");
+  Group G(ctxs, ctxs + nslabs);
+  std::vector<int64_t> n(nslabs);
+  std::vector<const double* const*> b(nslabs);
+  for (int i = 0; i < nslabs; ++i) {
+    n[i] = 2 * G[i]->grid.nloc;
+    b[i] = basis + (size_t)i * (k + 2);
+  }
+  return arnoldi_group(G, n.data(), b.data(), k, w, scale, h_host, broke);
 }
 
 int uc_combine(uc_ctx* c, int64_t n, const double* const* basis, int k, const double* y,

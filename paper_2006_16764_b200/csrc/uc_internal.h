@@ -3,6 +3,7 @@
 
 #include <cuda_runtime.h>
 
+#include <functional>
 #include <vector>
 
 #include "uc_common.cuh"
@@ -49,12 +50,38 @@ struct uc_ctx {
   unsigned int* flags = nullptr;      // [4] sticky status flags (device alias)
   unsigned int* flags_host = nullptr; // mapped pinned host memory
   unsigned long long* locate_key = nullptr;
-  // ghost planes [slot][side] -> [2][plane]
-  double* ghost[4][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr}};
+  // ghost planes [slot][side] -> [2][plane]; slots 0 u, 1 old, 2 prev, 3 v, 4 state
+  double* ghost[5][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr},
+                         {nullptr, nullptr}, {nullptr, nullptr}};
   uc::Precond* pc = nullptr;
+  // slab neighbours: a local context (same process/device) or a remote NCCL rank
+  uc_ctx* lo_local = nullptr;
+  uc_ctx* hi_local = nullptr;
+  int lo_rank = -1, hi_rank = -1;
+  bool dist = false;  // member of a multi-rank NCCL communicator
 };
 
 namespace uc {
+typedef std::vector<uc_ctx*> Group;
+
+// Addresses of the boundary / ghost planes of one logical vector per slab.
+struct PlaneAddr {
+  int nblocks = 2;
+  std::function<int64_t(uc_ctx*)> count;
+  std::function<const double*(uc_ctx*, int)> top, bottom;
+  std::function<double*(uc_ctx*, int)> glo, ghi;
+  // owned planes [slo, shi) of this vector's level; plane_ok filters which
+  // boundary planes move (by global plane index); unset = all
+  std::function<int64_t(uc_ctx*)> slo, shi;
+  std::function<bool(int64_t)> plane_ok;
+};
+// comm.cu
+bool group_has_remote(const Group& g);
+int exchange(const Group& g, const PlaneAddr& addr, bool dir_up, bool dir_down, cudaStream_t s);
+int global_sum(const Group& g, double* const* slots, bool do_sqrt, cudaStream_t s);
+bool group_needs_sum(const Group& g);
+// exchange ghost planes of unpadded block vectors vecs[i] into ghost slot `slot`
+int halo_vectors(const Group& g, int slot, const double* const* vecs, cudaStream_t s);
 // blas.cu
 int reduce_dot(uc_ctx* c, int64_t n, const double* a, const double* b, double* out_dev,
                bool sqrt_result);
@@ -71,6 +98,9 @@ int locate_nonfinite(uc_ctx* c, const uc_scheme* sc, int part, const double* u,
                      const double* old, const double* prev, int64_t out[5]);
 // precond.cu
 int precond_build(uc_ctx* c, const uc_scheme* sc, const double* state, const uc_precond_cfg* cfg);
+int precond_build_group(const Group& G, const uc_scheme* sc, const double* const* states,
+                        const uc_precond_cfg* cfg);
+int precond_apply_group(const Group& G, const double* const* v, double* const* out);
 int precond_apply(uc_ctx* c, const double* v, double* out);
 int precond_stencil(uc_ctx* c, int level, int block, double* host_out);
 int precond_levels(uc_ctx* c, int64_t* shapes);
