@@ -123,6 +123,10 @@ class TimestepResidual:
             return self.device_call(as_device(u_new))
         return to_host(self.device_call(as_device(u_new)))
 
+    def nonfinite(self) -> bool:
+        """Sticky non-finite flag of the last launches (synchronises)."""
+        return bool(self.ctx.status(clear=True).residual_nonfinite)
+
     def jv_device(self, u, fu, v, unorm: float, eps_out=None) -> torch.Tensor:
         """(F(u + eps v) - F(u)) / eps fused on the device (newton.py:107-113).
         Non-finite F(u+eps v) sets the sticky flag checked by the caller."""

@@ -179,3 +179,67 @@ def combine(basis, k: int, y: np.ndarray) -> torch.Tensor:
 
 def all_finite(x: torch.Tensor) -> bool:
     return bool(torch.isfinite(x).all().item()) if x.numel() else True
+
+
+def any_nonzero(x: torch.Tensor) -> bool:
+    return bool(torch.any(x != 0).item())
+
+
+def arnoldi(apply_op, basis: list, k: int, scale: float):
+    """One Arnoldi step (krylov.py:48-70) on device vectors: (h numpy, new
+    vector or None, breakdown)."""
+    w = as_device(apply_op(basis[k]))
+    if any(w.data_ptr() == b.data_ptr() for b in basis[: k + 1]):
+        w = w.clone()  # MGS updates w in place; never alias a basis vector
+    slot = torch.empty_like(w)
+    h = np.zeros(k + 2)
+    broke = C.c_int()
+    ctx = blas()
+    L.check(ctx.lib.uc_arnoldi(ctx.bind(), w.numel(), L.ptrs(basis[: k + 1] + [slot]), k, L.ptr(w),
+                               float(scale), h.ctypes.data_as(C.POINTER(C.c_double)), C.byref(broke)),
+            "uc_arnoldi")
+    if broke.value:
+        return h, None, True
+    return h, slot, False
+
+
+class DeviceSpace:
+    """Vector space of single contiguous fp64 CUDA tensors (one GPU)."""
+
+    def vec(self, x):
+        return as_device(x)
+
+    norm = staticmethod(norm)
+    dot = staticmethod(dot)
+    sub = staticmethod(sub)
+    div = staticmethod(div)
+    scale = staticmethod(scale)
+    combine = staticmethod(combine)
+    all_finite = staticmethod(all_finite)
+    any_nonzero = staticmethod(any_nonzero)
+    arnoldi = staticmethod(arnoldi)
+
+    @staticmethod
+    def axpy(a, s, b):
+        return axpy(a, s, b)
+
+    @staticmethod
+    def zeros_like(x):
+        return torch.zeros_like(x)
+
+    @staticmethod
+    def clone(x):
+        return x.clone()
+
+    @staticmethod
+    def is_native(x) -> bool:
+        return is_device(x)
+
+
+DEVICE = DeviceSpace()
+
+
+def space_of(x):
+    """The vector space a vector belongs to (slab vectors carry theirs)."""
+    sp = getattr(x, "space", None)
+    return sp if sp is not None else DEVICE
