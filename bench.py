@@ -197,6 +197,75 @@ def vcycle_bytes(pc, N, dim):
     return 2 * total  # both field blocks
 
 
+def run_slabs(args, w, rank, world, local, dist):
+    """N > 1: one slab per GPU of a weak-scaled mesh (counts[-1] x world), NCCL
+    ghost planes and allreduce inside the library (paper_2006_16764_b200.parallel)."""
+    import torch
+
+    import paper_2006_16764_b200 as uc
+    from paper_2006_16764_b200.parallel import SlabGroup, SlabResidual
+
+    dev = torch.device("cuda", local)
+    counts = list(w["counts"])
+    extents = list(w["extents"])
+    counts[-1] *= world
+    extents[-1] *= world
+    mesh = uc.build_mesh(w["dim"], extents, counts)
+    kern = uc.FreeGrowthKernel() if w["model"] == "free_growth" else uc.AlloyKernel()
+    sc = uc.ThetaScheme(w["theta"], w["dt"], w["step"])
+    grp = SlabGroup.from_torch_dist(mesh, kern)
+    lo, hi = grp.slabs[0]
+    nloc = (hi - lo) * grp.plane
+    rng = np.random.default_rng(11 + rank)
+    if w["model"] == "free_growth":
+        mk = lambda: np.concatenate([0.5 + 0.3 * rng.standard_normal(nloc), 1.0 + 0.2 * rng.standard_normal(nloc)])  # noqa: E731
+    else:
+        mk = lambda: np.concatenate([np.tanh(rng.standard_normal(nloc)), -0.5 + 0.4 * rng.standard_normal(nloc)])  # noqa: E731
+    sp = grp.space
+    u, old, prev = (sp.wrap([torch.from_numpy(mk()).to(dev)]) for _ in range(3))
+    v = sp.wrap([torch.from_numpy(np.random.default_rng(2 + rank).standard_normal(2 * nloc)).to(dev)])
+    res = SlabResidual(grp, old, prev, sc)
+    unorm = sp.norm(u)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        f = res.device_call(u, check=False)
+        return res.jv_device(u, f, v, unorm)
+
+    clk = Clocks(local).__enter__()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(args.steps):
+        step()
+    b.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk.__exit__()
+    t = torch.tensor([a.elapsed_time(b) / args.steps], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    D_glob = 2 * int(np.prod([c + 1 for c in counts]))
+    value = 2 * D_glob / (ms * 1e-3) / 1e6
+    if rank == 0:
+        line = {
+            "metric": "MDoF/s residual+Jv fill", "value": round(value, 2), "unit": "MDoF/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": args.workload, "model": w["model"], "dim": w["dim"], "counts": counts,
+                       "dof": D_glob, "dof_per_step": 2 * D_glob,
+                       "parallelism": f"slab x{world} (NCCL ghost planes + allreduce)",
+                       "l2": "per-rank inputs larger than L2; no flush"},
+            "gpu_launches": 3 * args.steps, "clocks": clk.summary(), "roofline": None,
+            "e2e": None, "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -226,6 +295,9 @@ def main():
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        run_slabs(args, w, rank, world, local, dist)
+        dist.destroy_process_group()
+        return
 
     import paper_2006_16764_b200 as uc
     from paper_2006_16764_b200 import device as D

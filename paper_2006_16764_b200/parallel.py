@@ -287,18 +287,20 @@ class SlabResidual:
     def fixed_part(self):
         return self._fixed
 
-    def __call__(self, u):
+    def device_call(self, u, check: bool = True):
         self.evaluations += 1
-        u = self.group.space.vec(u)
         out = self.group.space.wrap([torch.empty_like(p) for p in u.parts])
         n = len(u.parts)
         L.check(L.load().uc_residual_group(self.group.handles, n, C.byref(self._sc), L.UC_PART_NEW,
                                            L.ptrs(u.parts), L.ptrs(self.old.parts),
                                            L.ptrs(self.prev.parts), L.ptrs(self._fixed.parts),
                                            L.ptrs(out.parts)), "uc_residual_group(new)")
-        if self.group.flag("residual_nonfinite"):
+        if check and self.group.flag("residual_nonfinite"):
             raise NonFiniteResidualError("non-finite residual entry after assembly")
         return out
+
+    def __call__(self, u):
+        return self.device_call(self.group.space.vec(u))
 
     def jv_device(self, u, fu, v, unorm, eps_out=None):
         self.evaluations += 1
