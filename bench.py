@@ -71,33 +71,55 @@ def synthetic_states(w, seed=11):
 
 
 class Clocks:
-    """nvidia-smi sampler for the timed region (B200_PROFILING.md clocks line)."""
-
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap,utilization.gpu")
+    """SM clock and throttle-reason sampler for the timed region (NVML every
+    ~10 ms; the B200_PROFILING.md clocks line via nvidia-smi as a fallback)."""
 
     def __init__(self, index):
         self.index = index
         self.rows = []
         self._stop = threading.Event()
         self._t = None
+        self.source = "nvml"
 
     def _run(self):
-        while not self._stop.is_set():
-            try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True,
-                                     text=True, timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([s.strip() for s in out.split(",")])
-            except Exception:
-                pass
-            self._stop.wait(0.2)
+        try:
+            import pynvml as N
+
+            N.nvmlInit()
+            h = N.nvmlDeviceGetHandleByIndex(self.index)
+            mx = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
+            bits = {"hw_slowdown": N.nvmlClocksThrottleReasonHwSlowdown,
+                    "hw_thermal_slowdown": N.nvmlClocksThrottleReasonHwThermalSlowdown,
+                    "sw_thermal_slowdown": N.nvmlClocksThrottleReasonSwThermalSlowdown,
+                    "sw_power_cap": N.nvmlClocksThrottleReasonSwPowerCap}
+            while not self._stop.is_set():
+                sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+                r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.rows.append((float(sm), float(mx), [k for k, b in bits.items() if r & b]))
+                self._stop.wait(0.01)
+            N.nvmlShutdown()
+        except Exception:
+            self.source = "nvidia-smi"
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True,
+                                         text=True, timeout=5).stdout.strip().split(",")
+                    if len(out) >= 6:
+                        self.rows.append((float(out[0]), float(out[1]),
+                                          [names[i] for i in range(4) if out[2 + i].strip().lower() == "active"]))
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
 
     def __enter__(self):
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
+        time.sleep(0.05)
         return self
 
     def __exit__(self, *a):
@@ -107,14 +129,10 @@ class Clocks:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        sm = [r[0] for r in self.rows]
+        reasons = sorted({x for r in self.rows for x in r[2]})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": reasons, "samples": len(self.rows), "source": self.source}
 
 
 def cpu_oracle_step_time(w, steps=2, warmup=1, rows=None):
@@ -440,10 +458,25 @@ def main():
             t_newton = walls[-1]
             t_apply = timed(lambda: pc.device_apply(v, check=False), 5)
             vb = vcycle_bytes(pc, N, w["dim"])
+            pc = r0 = None
+            # full implicit time steps (precond build + Newton) through the host loop
+            from paper_2006_16764_b200.stepper import run_steps
+            step_walls = []
+            state = st
+            prev_state = st
+            for n in range(3):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                state_new, recs = run_steps(mesh, kern, state, 1, 0.5, w["dt"], startup_steps=0)
+                torch.cuda.synchronize()
+                step_walls.append(time.perf_counter() - t0)
+                state = state_new
             newton = {"sec_per_newton_iteration": round(t_newton / max(rep.iterations, 1), 5),
                       "newton_iterations": rep.iterations, "gmres_per_newton": rep.gmres_iterations,
                       "converged": bool(rep.converged), "precond_build_s": round(t_build, 4),
                       "cold_sec_per_newton_iteration": round(walls[0] / max(rep.iterations, 1), 5),
+                      "sec_per_time_step": round(float(np.mean(step_walls[1:])), 5),
+                      "time_step_walls_s": [round(x, 5) for x in step_walls],
                       "vcycle_apply_ms": round(t_apply, 3),
                       "vcycle_gbs": round(vb / (t_apply * 1e-3) / 1e9, 1),
                       "vcycle_hbm_frac": round(vb / (t_apply * 1e-3) / 1e9 / hbm_peak, 4),

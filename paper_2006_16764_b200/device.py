@@ -92,6 +92,10 @@ def _params_key(mp: L.ModelParams):
     return tuple(getattr(mp, f) for f, _ in L.ModelParams._fields_)
 
 
+def context_key(mesh, kernel, slab=None):
+    return (mesh_descriptor(mesh, slab), _params_key(device_params(kernel)), torch.cuda.current_device())
+
+
 def context_for(mesh, kernel, slab=None, fresh: bool = False) -> Context:
     """Shared (cached) context for a mesh/model pair, or a private one."""
     desc = mesh_descriptor(mesh, slab)

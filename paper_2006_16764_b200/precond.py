@@ -20,6 +20,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import warnings
+import weakref
 from dataclasses import dataclass
 
 import numpy as np
@@ -34,6 +35,22 @@ __all__ = ["PrecondConfig", "BlockPrecond", "build_precond", "apply_precond"]
 _KINDS = {"identity": L.UC_PC_IDENTITY, "jacobi": L.UC_PC_JACOBI, "sgs": L.UC_PC_SGS,
           "vcycle": L.UC_PC_VCYCLE}
 _warned = False
+
+# Contexts of dropped preconditioners, by (mesh, model): the next build on the
+# same mesh reuses its level buffers and captured graph (csrc/precond.cu).
+_pool: dict = {}
+
+
+def _pool_take(mesh, kernel):
+    key = D.context_key(mesh, kernel)
+    free = _pool.get(key)
+    if free:
+        return free.pop(), key
+    return D.context_for(mesh, kernel, fresh=True), key
+
+
+def _pool_give(key, ctx):
+    _pool.setdefault(key, []).append(ctx)
 
 
 @dataclass
@@ -88,12 +105,13 @@ class _BlockView:
     """Read-only view of one field block's level hierarchy (host copies)."""
 
     def __init__(self, pc, block):
-        self._pc = pc
+        self._pc = weakref.ref(pc)  # no reference cycle: the pool recycles on drop
         self._block = block
 
     @property
     def mats(self):
-        return [self._pc.level_matrix(lvl, self._block) for lvl in range(self._pc.n_levels)]
+        pc = self._pc()
+        return [pc.level_matrix(lvl, self._block) for lvl in range(pc.n_levels)]
 
 
 class BlockPrecond:
@@ -159,7 +177,7 @@ def build_precond(mesh, kernel, state, scheme, config: PrecondConfig | None = No
             warnings.warn("ordering='lexicographic' is applied as the reference's multicolor "
                           "ordering on the device", RuntimeWarning, stacklevel=2)
             _warned = True
-    ctx = D.context_for(mesh, kernel, fresh=True)
+    ctx, key = _pool_take(mesh, kernel)
     st = D.as_device(state)
     pc = L.PrecondCfg()
     pc.kind = _KINDS[cfg.kind]
@@ -169,7 +187,9 @@ def build_precond(mesh, kernel, state, scheme, config: PrecondConfig | None = No
     if rc == L.UC_ERR_ARG:
         raise ValueError(ctx.lib.uc_last_error().decode())
     L.check(rc, "uc_precond_build")
-    return BlockPrecond(ctx, ctx.n_local, cfg, mesh.dim)
+    bp = BlockPrecond(ctx, ctx.n_local, cfg, mesh.dim)
+    weakref.finalize(bp, _pool_give, key, ctx)
+    return bp
 
 
 def apply_precond(precond: BlockPrecond, v):

@@ -50,6 +50,9 @@ def run_steps(mesh, kernel, state0, nsteps: int, theta: float, dt: float,
         u_new, rep = newton_solve(res, state, ncfg, precond_apply=pc.apply if pc else None)
         records.append(StepRecord(n, rep.iterations, rep.total_gmres, list(rep.gmres_iterations),
                                   rep.initial_norm, rep.final_norm, rep.converged))
+        # drop this step's preconditioner before the next build so its level
+        # buffers and captured graph are recycled (precond._pool)
+        pc = res = None
         if not rep.converged:
             break
         prev, state = state, u_new
