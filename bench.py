@@ -317,7 +317,10 @@ def main():
         dist.destroy_process_group()
         return
 
+    import ctypes as C
+
     import paper_2006_16764_b200 as uc
+    from paper_2006_16764_b200 import _lib as L
     from paper_2006_16764_b200 import device as D
     from paper_2006_16764_b200.models import seed_initial_condition
 
@@ -398,6 +401,20 @@ def main():
                 "kernel": f"k_residual<{w['dim']},{'FG' if w['model'] == 'free_growth' else 'ALLOY'},NEW>",
                 "bytes_per_dof": 32, "ms_per_launch": round(t_res, 4), "peak_source": peak_src,
                 "note": "fp64-issue-bound kernel; HBM fraction ceiling ~20-30% in 2D (DESIGN.md)"}
+    # FP64 roofline of the same kernel: DP instructions per element measured
+    # with ncu (profiles/r01/SUMMARY.md) over the measured DFMA issue rate
+    dp_per_elem = {("free_growth", 2): 1019, ("free_growth", 3): None, ("alloy", 2): None, ("alloy", 3): None}
+    ms_probe, dfma_rate = C.c_double(), C.c_double()
+    bl = D.blas()
+    L.check(bl.lib.uc_fp64_probe(bl.bind(), 20000, C.byref(ms_probe), C.byref(dfma_rate)), "uc_fp64_probe")
+    ne = int(np.prod(w["counts"]))
+    dpe = dp_per_elem.get((w["model"], w["dim"]))
+    fp64 = {"bound": "fp64", "peak_dp_inst_per_s": round(dfma_rate.value / 1e12, 3),
+            "peak_tflops_dfma": round(2 * dfma_rate.value / 1e12, 3), "unit": "T DP inst/s",
+            "dp_inst_per_element": dpe}
+    if dpe:
+        ach = dpe * ne / (t_res * 1e-3)
+        fp64.update({"achieved": round(ach / 1e12, 3), "frac": round(ach / dfma_rate.value, 4)})
     kernels = {"residual_ms": round(t_res, 4), "jv_ms": round(t_jv, 4),
                "residual_mdofs": round(Dof / (t_res * 1e-3) / 1e6, 1),
                "jv_mdofs": round(Dof / (t_jv * 1e-3) / 1e6, 1),
@@ -502,7 +519,7 @@ def main():
                        "counts": list(w["counts"]), "dof": Dof, "dof_per_step": 2 * Dof,
                        "l2": "inputs (~470 MB working set) larger than L2; no flush",
                        "parallelism": f"replicas x{world}"},
-            "roofline": roofline, "kernels": kernels, "e2e": e2e,
+            "roofline": roofline, "fp64_roofline": fp64, "kernels": kernels, "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(),
             "newton": newton, "cpu_baseline": cpu,
         }

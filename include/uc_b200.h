@@ -198,6 +198,10 @@ int uc_precond_apply(uc_ctx* ctx, const double* v, double* out);
 int uc_precond_stencil(uc_ctx* ctx, int level, int block, double* host_out);
 int uc_precond_levels(uc_ctx* ctx, int64_t* shapes /* [levels][3] */);
 
+/* FP64 issue-rate probe (DFMA chains over all SMs), for the FP64 roofline
+ * denominator; synchronises.  Not part of the reference interface. */
+int uc_fp64_probe(uc_ctx* ctx, int iters, double* ms_out, double* dfma_per_s);
+
 /* Sticky status flags (synchronises); clear=1 resets them. */
 int uc_status(uc_ctx* ctx, uc_status_t* out, int clear);
 

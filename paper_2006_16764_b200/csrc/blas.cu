@@ -351,3 +351,42 @@ int uc_scale(uc_ctx* c, int64_t n, double s, const double* a, double* out) {
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// FP64 issue-rate probe: 8 independent DFMA chains per thread, enough warps
+// per SM to cover the pipe latency.  Used by bench.py to measure the FP64
+// roofline denominator (not in MEASURED_PEAKS.json).
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_dfma_probe(int iters, double a, double b, double* out) {
+  double x[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) x[i] = threadIdx.x * 1e-3 + i;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) x[i] = fma(x[i], a, b);
+  }
+  double s = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) s += x[i];
+  if (s == 1.2345) out[0] = s;  // keep the chains alive
+}
+
+extern "C" int uc_fp64_probe(uc_ctx* c, int iters, double* ms_out, double* dfma_per_s) {
+  if (!c || iters < 1) return set_error(UC_ERR_ARG, "uc_fp64_probe: bad argument");
+  const int blocks = c->num_sms * 8;
+  cudaEvent_t e0, e1;
+  UC_CUDA_OK(cudaEventCreate(&e0));
+  UC_CUDA_OK(cudaEventCreate(&e1));
+  k_dfma_probe<<<blocks, 256, 0, c->stream>>>(iters / 10 + 1, 0.999999, 1e-9, c->scal);
+  UC_CUDA_OK(cudaEventRecord(e0, c->stream));
+  k_dfma_probe<<<blocks, 256, 0, c->stream>>>(iters, 0.999999, 1e-9, c->scal);
+  UC_CUDA_OK(cudaEventRecord(e1, c->stream));
+  UC_CUDA_OK(cudaEventSynchronize(e1));
+  float ms = 0.f;
+  UC_CUDA_OK(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  *ms_out = ms;
+  *dfma_per_s = (double)blocks * 256.0 * 8.0 * iters / (ms * 1e-3);
+  return UC_OK;
+}
