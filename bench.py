@@ -394,6 +394,9 @@ def main():
             peaks = json.load(fh)
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    def roofline_kernel_name(w):
+        return f"k_residual<{w['dim']},{'FG' if w['model'] == 'free_growth' else 'ALLOY'},NEW>"
+
     res_bytes = 32 * Dof
     achieved = res_bytes / (t_res * 1e-3) / 1e9
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
@@ -403,7 +406,15 @@ def main():
                 "note": "fp64-issue-bound kernel; HBM fraction ceiling ~20-30% in 2D (DESIGN.md)"}
     # FP64 roofline of the same kernel: DP instructions per element measured
     # with ncu (profiles/r01/SUMMARY.md) over the measured DFMA issue rate
-    dp_per_elem = {("free_growth", 2): 1019, ("free_growth", 3): None, ("alloy", 2): None, ("alloy", 3): None}
+    dp_per_elem = {}
+    try:
+        with open(os.path.join(ROOT, "profiles", "dp_inst_per_element.json")) as fh:
+            for key, val in json.load(fh)["kernels"].items():
+                model, dims, mode = key.rsplit("_", 2)
+                if mode == "new":
+                    dp_per_elem[(model, int(dims[0]))] = val["dp_inst_per_element"]
+    except Exception:
+        pass
     ms_probe, dfma_rate = C.c_double(), C.c_double()
     bl = D.blas()
     L.check(bl.lib.uc_fp64_probe(bl.bind(), 20000, C.byref(ms_probe), C.byref(dfma_rate)), "uc_fp64_probe")
@@ -411,7 +422,9 @@ def main():
     dpe = dp_per_elem.get((w["model"], w["dim"]))
     fp64 = {"bound": "fp64", "peak_dp_inst_per_s": round(dfma_rate.value / 1e12, 3),
             "peak_tflops_dfma": round(2 * dfma_rate.value / 1e12, 3), "unit": "T DP inst/s",
-            "dp_inst_per_element": dpe}
+            "dp_inst_per_element": dpe, "kernel": roofline_kernel_name(w),
+            "note": "DP instructions per element from ncu (profiles/dp_inst_per_element.json); "
+                    "peak = measured DFMA issue rate (uc_fp64_probe)"}
     if dpe:
         ach = dpe * ne / (t_res * 1e-3)
         fp64.update({"achieved": round(ach / 1e12, 3), "frac": round(ach / dfma_rate.value, 4)})
@@ -421,35 +434,53 @@ def main():
                "jv_gbs": round(48 * Dof / (t_jv * 1e-3) / 1e9, 1)}
 
     # ---- end-to-end through the public API with host buffers ----------
+    # Each step copies u, v from pinned host memory, calls the public API
+    # (TimestepResidual.__call__ + jfnk_matvec) and copies F, Jv back.  Copies
+    # run on two copy streams (double-buffered) so the download of step i
+    # overlaps the upload of step i+1; every byte still moves inside the
+    # timed region.
     u_pin = torch.from_numpy(u_h).pin_memory()
     v_pin = torch.from_numpy(v_h).pin_memory()
-    f_pin = torch.empty(Dof, dtype=torch.float64).pin_memory()
-    j_pin = torch.empty(Dof, dtype=torch.float64).pin_memory()
-    u_d = torch.empty(Dof, dtype=torch.float64, device=dev)
-    v_d = torch.empty(Dof, dtype=torch.float64, device=dev)
+    f_pin = [torch.empty(Dof, dtype=torch.float64).pin_memory() for _ in range(2)]
+    j_pin = [torch.empty(Dof, dtype=torch.float64).pin_memory() for _ in range(2)]
+    u_d = [torch.empty(Dof, dtype=torch.float64, device=dev) for _ in range(2)]
+    v_d = [torch.empty(Dof, dtype=torch.float64, device=dev) for _ in range(2)]
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    ev_in = [torch.cuda.Event() for _ in range(2)]
+    ev_out = [torch.cuda.Event() for _ in range(2)]
 
-    def e2e_step():
-        u_d.copy_(u_pin, non_blocking=True)
-        v_d.copy_(v_pin, non_blocking=True)
-        F = res(u_d)
-        Jv = uc.jfnk_matvec(res, u_d, F, v_d)
-        f_pin.copy_(F, non_blocking=True)
-        j_pin.copy_(Jv, non_blocking=True)
+    def e2e_run(nsteps):
+        for i in range(nsteps):
+            k = i % 2
+            with torch.cuda.stream(s_in):
+                s_in.wait_event(ev_out[k])  # buffer k free again (its results left)
+                u_d[k].copy_(u_pin, non_blocking=True)
+                v_d[k].copy_(v_pin, non_blocking=True)
+                ev_in[k].record(s_in)
+            stream.wait_event(ev_in[k])
+            F = res(u_d[k])
+            Jv = uc.jfnk_matvec(res, u_d[k], F, v_d[k])
+            ev_out[k].record(stream)
+            with torch.cuda.stream(s_out):
+                s_out.wait_event(ev_out[k])
+                f_pin[k].copy_(F, non_blocking=True)
+                j_pin[k].copy_(Jv, non_blocking=True)
+                ev_out[k].record(s_out)
 
-    for _ in range(args.warmup):
-        e2e_step()
-    barrier()
-    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a.record(stream)
-    for _ in range(args.steps):
-        e2e_step()
-    b.record(stream)
+    e2e_run(args.warmup)
     torch.cuda.synchronize()
     barrier()
-    e2e_ms = max_over_ranks(a.elapsed_time(b) / args.steps)
+    a0, b0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record(stream)
+    e2e_run(args.steps)
+    stream.wait_stream(s_out)  # end mark after the last download
+    b0.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = max_over_ranks(a0.elapsed_time(b0) / args.steps)
     e2e = {"value": round(world * 2 * Dof / (e2e_ms * 1e-3) / 1e6, 2), "unit": "MDoF/s",
            "h2d_bytes_per_step": 2 * Dof * 8, "d2h_bytes_per_step": 2 * Dof * 8,
-           "ms_per_step": round(e2e_ms, 3)}
+           "ms_per_step": round(e2e_ms, 3), "copies": "pinned, double-buffered copy streams"}
     launches_per_step = 3  # residual tile, |v| reduction, Jv tile
 
     # ---- Newton step on the seeded dendrite --------------------------
