@@ -198,6 +198,14 @@ int uc_precond_apply(uc_ctx* ctx, const double* v, double* out);
 int uc_precond_stencil(uc_ctx* ctx, int level, int block, double* host_out);
 int uc_precond_levels(uc_ctx* ctx, int64_t* shapes /* [levels][3] */);
 
+/* On-device initial conditions over the context's owned planes (SURVEY 8(f)
+ * #4).  kind 0 = seed_initial_condition (free_growth.py:249-265), params
+ * {anisotropy_strength, radius, far_temperature}; kind 1 =
+ * directional_initial_condition (alloy.py:317-357), params {interface_x0,
+ * amplitude, seed, smooth}.  extents[dim] are the mesh extents. */
+int uc_initial_state(uc_ctx* ctx, int kind, const double* extents, const double* params,
+                     double* out);
+
 /* FP64 issue-rate probe (DFMA chains over all SMs), for the FP64 roofline
  * denominator; synchronises.  Not part of the reference interface. */
 int uc_fp64_probe(uc_ctx* ctx, int iters, double* ms_out, double* dfma_per_s);

@@ -80,6 +80,7 @@ SIGNATURES = {
     "uc_precond_levels": (_I, [_P, C.POINTER(_I64)]),
     "uc_status": (_I, [_P, C.POINTER(Status), _I]),
     "uc_fp64_probe": (_I, [_P, _I, C.POINTER(_D), C.POINTER(_D)]),
+    "uc_initial_state": (_I, [_P, _I, C.POINTER(_D), C.POINTER(_D), _P]),
     "uc_nccl_unique_id": (_I, [C.c_char_p, _P]),
     "uc_comm_init_nccl": (_I, [C.c_char_p, _P, _I, _I]),
     "uc_comm_finalize": (_I, []),

@@ -257,3 +257,36 @@ def directional_initial_condition(mesh, params: AlloyParams, amplitude: float = 
     else:
         phi = np.where(x <= threshold, 1.0, -1.0)
     return np.concatenate([phi, np.full(mesh.n_nodes, -1.0)])
+
+
+def _device_initial(ctx, mesh, kind, params):
+    import ctypes as C
+
+    import torch
+
+    ext = (C.c_double * 3)(*(list(mesh.extents) + [1.0] * (3 - mesh.dim)))
+    par = (C.c_double * 4)(*(list(params) + [0.0] * (4 - len(params))))
+    out = torch.empty(2 * ctx.n_local, dtype=torch.float64, device="cuda")
+    L.check(ctx.lib.uc_initial_state(ctx.bind(), kind, ext, par, L.ptr(out)), "uc_initial_state")
+    return out
+
+
+def seed_initial_condition_device(mesh, params: FreeGrowthParams, radius: float | None = None, ctx=None):
+    """seed_initial_condition generated on the GPU (no host coordinate array);
+    with `ctx` (a slab context) only that slab's planes."""
+    from .device import context_for
+
+    r = params.seed_radius if radius is None else radius
+    if r <= 0.0:
+        raise ValueError("seed radius must be positive")
+    ctx = ctx or context_for(mesh, FreeGrowthKernel(params))
+    return _device_initial(ctx, mesh, 0, (params.anisotropy_strength, r, params.far_temperature))
+
+
+def directional_initial_condition_device(mesh, params: AlloyParams, amplitude: float = 0.0,
+                                         seed: int = 0, smooth: bool = False, ctx=None):
+    """directional_initial_condition generated on the GPU."""
+    from .device import context_for
+
+    ctx = ctx or context_for(mesh, AlloyKernel(params))
+    return _device_initial(ctx, mesh, 1, (params.interface_x0, amplitude, float(seed), 1.0 if smooth else 0.0))
