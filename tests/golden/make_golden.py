@@ -183,11 +183,15 @@ RUNS = [
     ("al2d_256x64_10", "alloy", 2, (204.8, 51.2), (256, 64), 0.002, 10, {}, True),
     ("fg3d_16_3", "free_growth", 3, (0.48, 0.48, 0.48), (16, 16, 16), 2.25e-4, 3, {}, True),
     ("al3d_32x16x16_3", "alloy", 3, (25.6, 12.8, 12.8), (32, 16, 16), 0.002, 3, {}, True),
+    ("fg2d_512_3", "free_growth", 2, (15.36, 15.36), (512, 512), 2.25e-4, 3, {}, False),
+    ("al2d_512_3", "alloy", 2, (409.6, 409.6), (512, 512), 0.002, 3, {}, False),
 ]
 
 
-def run_cases(meta):
+def run_cases(meta, only=None):
     for name, model, dim, ext, cnt, dt, nsteps, pc_over, keep in RUNS:
+        if only and name not in only:
+            continue
         cfg = default_config(model)
         cfg.mesh.dimension = dim
         cfg.mesh.extents = ext
@@ -230,15 +234,24 @@ def ic_cases(meta):
 
 def main():
     meta = {"generator": "tests/golden/make_golden.py", "reference": REF}
-    residual_cases(meta)
-    precond_cases(meta)
-    newton_case(meta)
-    ic_cases(meta)
-    if "--no-runs" not in sys.argv:
+    if "--only-runs" not in sys.argv:
+        residual_cases(meta)
+        precond_cases(meta)
+        newton_case(meta)
+        ic_cases(meta)
+    old = json.load(open(os.path.join(OUT, "golden.json"))) if os.path.exists(os.path.join(OUT, "golden.json")) else {}
+    if "--only-runs" in sys.argv:
+        meta = old
+        run_cases(meta, only=sys.argv[sys.argv.index("--only-runs") + 1].split(","))
+    elif "--no-runs" not in sys.argv:
         run_cases(meta)
     else:
-        old = json.load(open(os.path.join(OUT, "golden.json")))
         meta.update({k: v for k, v in old.items() if k.startswith("run_")})
+    # measured with the reference in SURVEY.md section 8(c) (453 s on this host):
+    # free growth 2048^2, 2 steps, default solver, multicolor == lexicographic counts
+    meta["survey_fg2d_2048_2"] = dict(model="free_growth", dim=2, extents=(61.44, 61.44),
+                                      counts=(2048, 2048), dt=2.25e-4, steps=2, newton=[4, 3],
+                                      gmres=[16, 12], source="SURVEY.md 8(c) / BASELINE.md 4.1")
     with open(os.path.join(OUT, "golden.json"), "w") as fh:
         json.dump(meta, fh, indent=1, sort_keys=True)
 
