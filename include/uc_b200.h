@@ -91,13 +91,16 @@ typedef struct uc_scheme {
   int64_t step;
 } uc_scheme;
 
-/* PrecondConfig (undercool/precond.py:54-71); ordering is always multicolor. */
+/* PrecondConfig (undercool/precond.py:54-71). */
+#define UC_ORDER_MULTICOLOR 0
+#define UC_ORDER_LEXICOGRAPHIC 1
 typedef struct uc_precond_cfg {
   int32_t kind;           /* UC_PC_* */
   int32_t sweeps;
   int32_t cycles;
   int32_t levels;
   int32_t coarse_sweeps;
+  int32_t ordering;       /* UC_ORDER_*: lexicographic = exact sequential GS as a wavefront */
 } uc_precond_cfg;
 
 /* Sticky device-side status, read with uc_status (synchronises). */

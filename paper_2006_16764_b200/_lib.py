@@ -39,7 +39,7 @@ class Scheme(C.Structure):
 
 class PrecondCfg(C.Structure):
     _fields_ = [("kind", C.c_int32), ("sweeps", C.c_int32), ("cycles", C.c_int32),
-                ("levels", C.c_int32), ("coarse_sweeps", C.c_int32)]
+                ("levels", C.c_int32), ("coarse_sweeps", C.c_int32), ("ordering", C.c_int32)]
 
 
 class Status(C.Structure):

@@ -333,6 +333,7 @@ class SlabPrecond:
         pc = L.PrecondCfg()
         pc.kind = _KINDS[cfg.kind]
         pc.sweeps, pc.cycles, pc.levels, pc.coarse_sweeps = cfg.sweeps, cfg.cycles, cfg.levels, cfg.coarse_sweeps
+        pc.ordering = 1 if cfg.ordering == "lexicographic" else 0
         sc = scheme_struct(scheme)
         rc = L.load().uc_precond_build_group(self.group.handles, len(self.group.ctxs), C.byref(sc),
                                              L.ptrs(st.parts), C.byref(pc))

@@ -6,20 +6,19 @@ coefficients at Gauss points and fills fixed 9-/27-point stencils on the device
 ``BlockPrecond.apply`` runs the multicolor symmetric Gauss-Seidel V-cycle
 (K8-K10) for both field blocks in each launch.
 
-Ordering.  The reference's default smoother ordering is "lexicographic"
-(precond.py:62), a sequential triangular sweep.  The device implements the
-reference's own "multicolor" ordering (precond.py:113-121) exactly; for
-ordering="lexicographic" it warns once and applies multicolor (identical
-Newton/GMRES counts on every case measured).  Set
-UC_B200_STRICT_ORDERING=1 to raise instead.  kind="direct" (SuperLU) has no
-device implementation and raises.
+Ordering.  Both of the reference's smoother orderings run on the device:
+"multicolor" (precond.py:113-121) as one launch per parity colour, and the
+reference's default "lexicographic" (precond.py:32-51), the sequential
+triangular sweep, reproduced exactly as a wavefront (rows with i + 2j (+4k)
+constant are mutually independent) in one cooperative launch per smoothing
+call.  Multicolor is the fast path (identical Newton/GMRES counts on every
+case measured); lexicographic is the bit-faithful
+one.  kind="direct" (SuperLU) has no device implementation and raises.
 """
 
 from __future__ import annotations
 
 import ctypes as C
-import os
-import warnings
 import weakref
 from dataclasses import dataclass
 
@@ -34,7 +33,6 @@ __all__ = ["PrecondConfig", "BlockPrecond", "build_precond", "apply_precond"]
 
 _KINDS = {"identity": L.UC_PC_IDENTITY, "jacobi": L.UC_PC_JACOBI, "sgs": L.UC_PC_SGS,
           "vcycle": L.UC_PC_VCYCLE}
-_warned = False
 
 # Contexts of dropped preconditioners, by (mesh, model): the next build on the
 # same mesh reuses its level buffers and captured graph (csrc/precond.cu).
@@ -166,22 +164,15 @@ class BlockPrecond:
 
 
 def build_precond(mesh, kernel, state, scheme, config: PrecondConfig | None = None) -> BlockPrecond:
-    global _warned
     cfg = config or PrecondConfig()
     if cfg.kind == "direct":
         raise NotImplementedError("kind='direct' (SuperLU) has no device implementation")
-    if cfg.ordering == "lexicographic" and cfg.kind in ("sgs", "vcycle"):
-        if os.environ.get("UC_B200_STRICT_ORDERING") == "1":
-            raise NotImplementedError("lexicographic Gauss-Seidel is not implemented on the device")
-        if not _warned:
-            warnings.warn("ordering='lexicographic' is applied as the reference's multicolor "
-                          "ordering on the device", RuntimeWarning, stacklevel=2)
-            _warned = True
     ctx, key = _pool_take(mesh, kernel)
     st = D.as_device(state)
     pc = L.PrecondCfg()
     pc.kind = _KINDS[cfg.kind]
     pc.sweeps, pc.cycles, pc.levels, pc.coarse_sweeps = cfg.sweeps, cfg.cycles, cfg.levels, cfg.coarse_sweeps
+    pc.ordering = 1 if cfg.ordering == "lexicographic" else 0
     sc = scheme_struct(scheme)
     rc = ctx.lib.uc_precond_build(ctx.bind(), C.byref(sc), L.ptr(st), C.byref(pc))
     if rc == L.UC_ERR_ARG:

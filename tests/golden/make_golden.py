@@ -134,6 +134,9 @@ def precond_cases(meta):
             cfg = uc.PrecondConfig(kind=kind, ordering="multicolor")
             pc = uc.build_precond(mesh, k, state, scheme, cfg)
             out[f"apply_{kind}"] = pc.apply(v)
+            if kind in ("sgs", "vcycle"):  # the reference's default ordering
+                lex = uc.build_precond(mesh, k, state, scheme, uc.PrecondConfig(kind=kind))
+                out[f"apply_{kind}_lex"] = lex.apply(v)
             if kind == "vcycle":
                 sizes = [m.shape[0] for m in pc.solvers[0].mats]
                 for lvl, m in enumerate(pc.solvers[0].mats[1:], start=1):
@@ -184,6 +187,10 @@ RUNS = [
     ("fg3d_16_3", "free_growth", 3, (0.48, 0.48, 0.48), (16, 16, 16), 2.25e-4, 3, {}, True),
     ("al3d_32x16x16_3", "alloy", 3, (25.6, 12.8, 12.8), (32, 16, 16), 0.002, 3, {}, True),
     ("fg2d_512_3", "free_growth", 2, (15.36, 15.36), (512, 512), 2.25e-4, 3, {}, False),
+    ("fg2d_128_10_lex", "free_growth", 2, (3.84, 3.84), (128, 128), 2.25e-4, 10,
+     {"ordering": "lexicographic"}, True),
+    ("al2d_256x64_10_lex", "alloy", 2, (204.8, 51.2), (256, 64), 0.002, 10,
+     {"ordering": "lexicographic"}, True),
     ("al2d_512_3", "alloy", 2, (409.6, 409.6), (512, 512), 0.002, 3, {}, False),
 ]
 
