@@ -209,6 +209,34 @@ int uc_precond_levels(uc_ctx* ctx, int64_t* shapes /* [levels][3] */);
 int uc_initial_state(uc_ctx* ctx, int kind, const double* extents, const double* params,
                      double* out);
 
+/* Per-step diagnostics of the time loop, replacing the host
+ * passes of undercool/driver.py:186-229 over the new state:
+ *   out[0] number of non-finite entries of unew      (driver.py:186)
+ *   out[1] max |unew|                                (driver.py:187, BLOWUP_LIMIT)
+ *   out[2..4] w@(T_new-T_old), w@(phi_new-phi_old), w@(phi_old-phi_prev)
+ *          with w = mesh.integration_weights()       (_heat_balance, driver.py:86-98)
+ *   out[5] composition integral at the new level     (_total_solute, driver.py:76-83)
+ *   out[6..7] x_tip, found along the first node row  (extract_tip, diagnostics.py:69-89)
+ * over the context's owned slab (`out` is a device array of UC_DIAG_N
+ * doubles, zero where not requested; the tip only on the slab holding plane
+ * 0).  Asynchronous on the context stream.  The group entry point exchanges
+ * the ghost plane the composition integral needs and writes one out array per
+ * slab; the caller adds the slab partials in slab order. */
+#define UC_DIAG_BALANCE 1
+#define UC_DIAG_SOLUTE 2
+#define UC_DIAG_TIP 4
+#define UC_DIAG_N 8
+typedef struct uc_diag_args {
+  int32_t what;                 /* UC_DIAG_* mask (non-finite and max are always computed) */
+  int32_t pad;
+  double elem_node_weight[8];   /* jxw @ values per local node (mesh.py:136) */
+  double composition;           /* AlloyParams.composition (map_u_to_c, alloy.py:119-127) */
+  double tip_level;             /* kernel.contour_level */
+  double extent_x;              /* mesh.extents[0] (last linspace node) */
+} uc_diag_args;
+int uc_step_diagnostics(uc_ctx* ctx, const double* unew, const double* old,
+                        const double* prev, const uc_diag_args* args, double* out);
+
 /* FP64 issue-rate probe (DFMA chains over all SMs), for the FP64 roofline
  * denominator; synchronises.  Not part of the reference interface. */
 int uc_fp64_probe(uc_ctx* ctx, int iters, double* ms_out, double* dfma_per_s);
@@ -250,6 +278,9 @@ int uc_precond_build_group(uc_ctx* const* ctxs, int n, const uc_scheme* sc,
                            const double* const* states, const uc_precond_cfg* cfg);
 int uc_precond_apply_group(uc_ctx* const* ctxs, int n, const double* const* v,
                            double* const* out);
+int uc_step_diagnostics_group(uc_ctx* const* ctxs, int n, const double* const* unew,
+                              const double* const* old, const double* const* prev,
+                              const uc_diag_args* args, double* const* out);
 
 #ifdef __cplusplus
 }

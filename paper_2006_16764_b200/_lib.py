@@ -42,6 +42,14 @@ class PrecondCfg(C.Structure):
                 ("levels", C.c_int32), ("coarse_sweeps", C.c_int32), ("ordering", C.c_int32)]
 
 
+class DiagArgs(C.Structure):
+    _fields_ = [("what", C.c_int32), ("pad", C.c_int32), ("elem_node_weight", C.c_double * 8),
+                ("composition", C.c_double), ("tip_level", C.c_double), ("extent_x", C.c_double)]
+
+
+DIAG_BALANCE, DIAG_SOLUTE, DIAG_TIP, DIAG_N = 1, 2, 4, 8
+
+
 class Status(C.Structure):
     _fields_ = [("residual_nonfinite", C.c_int32), ("precond_nonfinite", C.c_int32),
                 ("precond_bad_diag", C.c_int32), ("pad", C.c_int32)]
@@ -81,6 +89,7 @@ SIGNATURES = {
     "uc_status": (_I, [_P, C.POINTER(Status), _I]),
     "uc_fp64_probe": (_I, [_P, _I, C.POINTER(_D), C.POINTER(_D)]),
     "uc_initial_state": (_I, [_P, _I, C.POINTER(_D), C.POINTER(_D), _P]),
+    "uc_step_diagnostics": (_I, [_P, _P, _P, _P, C.POINTER(DiagArgs), _P]),
     "uc_nccl_unique_id": (_I, [C.c_char_p, _P]),
     "uc_comm_init_nccl": (_I, [C.c_char_p, _P, _I, _I]),
     "uc_comm_finalize": (_I, []),
@@ -96,6 +105,8 @@ SIGNATURES = {
     "uc_precond_build_group": (_I, [C.POINTER(_P), _I, C.POINTER(Scheme), C.POINTER(_P),
                                     C.POINTER(PrecondCfg)]),
     "uc_precond_apply_group": (_I, [C.POINTER(_P), _I, C.POINTER(_P), C.POINTER(_P)]),
+    "uc_step_diagnostics_group": (_I, [C.POINTER(_P), _I] + [C.POINTER(_P)] * 3
+                                  + [C.POINTER(DiagArgs), C.POINTER(_P)]),
 }
 
 _lock = threading.Lock()

@@ -50,6 +50,7 @@ struct uc_ctx {
   unsigned int* flags = nullptr;      // [4] sticky status flags (device alias)
   unsigned int* flags_host = nullptr; // mapped pinned host memory
   unsigned long long* locate_key = nullptr;
+  double* diag_ws = nullptr;      // diag.cu partials + ticket (lazy)
   // ghost planes [slot][side] -> [2][plane]; slots 0 u, 1 old, 2 prev, 3 v, 4 state
   double* ghost[5][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr},
                          {nullptr, nullptr}, {nullptr, nullptr}};

@@ -17,6 +17,8 @@ Reference entry points exercised (file:line under /root/reference/pkg/src/underc
   gmres_solve                  krylov.py:81-208
   newton_solve                 newton.py:116-198
   simulate (iteration counts)  driver.py:135-242
+  simulate records / outcomes  driver.py:186-229 (driver_cases)
+  _heat_balance, _total_solute driver.py:76-98, extract_tip diagnostics.py:69-89
 """
 
 from __future__ import annotations
@@ -239,8 +241,127 @@ def ic_cases(meta):
                       seed=dict(extents=(3.84, 3.84), counts=(128, 128)))
 
 
+def _rec_json(r):
+    out = {}
+    for key, val in r.items():
+        if isinstance(val, (np.floating, float)):
+            out[key] = float(val)
+        elif isinstance(val, (np.integer, int)):
+            out[key] = int(val)
+        else:
+            out[key] = val
+    return out
+
+
+def _small_fg(**time_kw):
+    # tests/test_driver.py:22-27
+    from undercool.config import MeshConfig, RunConfig, TimeConfig
+
+    cfg = RunConfig()
+    cfg.mesh = MeshConfig(dimension=2, extents=(0.96, 0.96), counts=(32, 32))
+    cfg.time = TimeConfig(**({"theta": 0.5, "dt": 1e-5, "t_final": 1e-4} | time_kw))
+    return cfg
+
+
+def driver_cases(meta):
+    """Full simulate() records and outcomes at the reference's own test configs
+    (tests/test_driver.py:22-27,118-163) with the default solver settings."""
+    from undercool.config import MeshConfig, TimeConfig
+
+    cases = {}
+    cases["fg2d_32_10"] = _small_fg()
+    cases["fg2d_32_balance6"] = _small_fg(dt=2.25e-4, t_final=2.25e-4 * 6)
+    cases["fg2d_32_explicit"] = _small_fg(theta=0.0, dt=5.625e-4, t_final=5.625e-4 * 50)
+    c = _small_fg(dt=2.25e-4, t_final=2.25e-4 * 2)
+    c.solver.max_iterations = 1
+    c.solver.rel_tol = 1e-14
+    cases["fg2d_32_starved"] = c
+    c = _small_fg(dt=2.25e-4, t_final=2.25e-4 * 2)
+    c.solver.max_iterations = 1
+    c.solver.rel_tol = 1e-14
+    c.retry_halve_dt = True
+    cases["fg2d_32_starved_retry"] = c
+    c = default_config("alloy")
+    c.mesh = MeshConfig(dimension=2, extents=(102.4, 25.6), counts=(128, 32))
+    c.time = TimeConfig(theta=0.5, dt=0.002, t_final=0.02)
+    cases["al2d_128x32_10"] = c
+    c = _small_fg(dt=2.25e-4, t_final=2.25e-4 * 3)
+    c.mesh = MeshConfig(dimension=3, extents=(0.48, 0.48, 0.48), counts=(16, 16, 16))
+    cases["fg3d_16_3"] = c
+    c = default_config("alloy")
+    c.mesh = MeshConfig(dimension=3, extents=(25.6, 12.8, 12.8), counts=(32, 16, 16))
+    c.time = TimeConfig(theta=0.5, dt=0.002, t_final=0.006)
+    cases["al3d_32x16x16_3"] = c
+    for name, cfg in cases.items():
+        t0 = time.perf_counter()
+        res = simulate(cfg)
+        m = dict(status=res.status, steps_completed=res.steps_completed,
+                 final_time=float(res.final_time), total_newton=res.total_newton,
+                 total_gmres=res.total_gmres, failure_detail=res.failure_detail,
+                 timescales={k: float(v) for k, v in res.timescales.items()},
+                 records=[_rec_json(r) for r in res.records],
+                 config=dict(model=cfg.model, dim=cfg.mesh.dimension, extents=list(cfg.mesh.extents),
+                             counts=list(cfg.mesh.counts), theta=cfg.time.theta, dt=cfg.time.dt,
+                             t_final=cfg.time.t_final, startup_dt=cfg.time.startup_dt,
+                             max_iterations=cfg.solver.max_iterations, rel_tol=cfg.solver.rel_tol,
+                             retry_halve_dt=cfg.retry_halve_dt),
+                 wall_seconds=time.perf_counter() - t0)
+        meta[f"driver_{name}"] = m
+        if res.status == "ok":
+            np.savez_compressed(os.path.join(OUT, f"driver_{name}.npz"), state=res.state)
+        print("driver", name, res.status, res.steps_completed, f"{m['wall_seconds']:.1f}s", flush=True)
+
+
+def diag_cases(meta):
+    """Diagnostics on the residual goldens' seeded states (driver.py:76-98,
+    diagnostics.py:69-89) plus tip profiles of the reference's tests."""
+    from undercool.diagnostics import extract_tip
+    from undercool.driver import _heat_balance, _total_solute
+
+    for name, model, dim, ext, cnt, th, dt, step, norm in RESIDUAL_CASES:
+        g = np.load(os.path.join(OUT, f"residual_{name}.npz"))
+        mesh = uc.build_mesh(dim, ext, cnt)
+        k = kernel_for(model, norm)
+        w = mesh.integration_weights()
+        n = mesh.n_nodes
+        new, old, prev = g["new"], g["old"], g["prev"]
+        d = dict(w_dT=float(w @ (new[n:] - old[n:])), w_dphi_new=float(w @ (new[:n] - old[:n])),
+                 w_dphi_old=float(w @ (old[:n] - prev[:n])), max_abs=float(np.max(np.abs(new))))
+        if model == "free_growth":
+            bal, bound = _heat_balance(mesh, k, StateHistory(new, old, prev), uc.ThetaScheme(th, dt, step), 0.25)
+            d.update(balance=bal, bound=bound)
+        else:
+            d["total_solute"] = _total_solute(mesh, k, new)
+        if dim == 2:
+            tip, found = extract_tip(new, mesh, k.contour_level, 2)
+            d.update(x_tip=float(tip), found=bool(found))
+        meta[f"diag_{name}"] = d
+    # tip profiles: step, tanh, no crossing, exact zero (tests/test_diagnostics.py)
+    mesh = uc.build_mesh(2, (4.5, 4.5), (150, 150))
+    xs = mesh.coords[:, 0]
+    profiles = {
+        "step": np.where(xs < 1.234, 1.0, 0.0),
+        "tanh": 0.5 * (1.0 - np.tanh((xs - 2.71) / 0.1)),
+        "none": np.ones_like(xs),
+        "exact": np.where(xs < 1.5, 1.0, np.where(np.isclose(xs, 1.5), 0.5, 0.0)),
+    }
+    tips = {}
+    for pname, phi in profiles.items():
+        state = uc.join_fields(phi, np.zeros(mesh.n_nodes))
+        tip, found = extract_tip(state, mesh, 0.5, 2)
+        tips[pname] = dict(x_tip=float(tip), found=bool(found))
+    meta["diag_tips_150"] = tips
+
+
 def main():
     meta = {"generator": "tests/golden/make_golden.py", "reference": REF}
+    if "--only-driver" in sys.argv:
+        meta = json.load(open(os.path.join(OUT, "golden.json")))
+        driver_cases(meta)
+        diag_cases(meta)
+        with open(os.path.join(OUT, "golden.json"), "w") as fh:
+            json.dump(meta, fh, indent=1, sort_keys=True)
+        return
     if "--only-runs" not in sys.argv:
         residual_cases(meta)
         precond_cases(meta)
@@ -252,6 +373,8 @@ def main():
         run_cases(meta, only=sys.argv[sys.argv.index("--only-runs") + 1].split(","))
     elif "--no-runs" not in sys.argv:
         run_cases(meta)
+        driver_cases(meta)
+        diag_cases(meta)
     else:
         meta.update({k: v for k, v in old.items() if k.startswith("run_")})
     # measured with the reference in SURVEY.md section 8(c) (453 s on this host):

@@ -100,3 +100,45 @@ def test_gauss_constants_bitwise_numpy():
     assert float.fromhex(lits["UC_LA"]) == (1.0 - x[0]) / 2.0
     assert float.fromhex(lits["UC_LB"]) == (1.0 + x[0]) / 2.0
     assert float.fromhex(lits["UC_EPS0"]) == np.sqrt(np.finfo(float).eps)
+
+
+def test_run_config_validation_mirrors_reference():
+    """config.py:74-97 checks run before any device work (tests/test_driver.py:60-72)."""
+    from paper_2006_16764_b200.config import MeshConfig, RunConfig, TimeConfig, default_config
+    from paper_2006_16764_b200.driver import simulate
+    from paper_2006_16764_b200.errors import ConfigError
+
+    for mutate in (lambda c: setattr(c, "model", "plasma"),
+                   lambda c: setattr(c.mesh, "counts", (4,)),
+                   lambda c: setattr(c.time, "theta", 2.0),
+                   lambda c: setattr(c.time, "dt", -1.0),
+                   lambda c: setattr(c.precond, "ordering", "random")):
+        cfg = RunConfig()
+        mutate(cfg)
+        with pytest.raises(ConfigError):
+            simulate(cfg)
+    a = default_config("alloy")
+    assert a.mesh == MeshConfig(dimension=2, extents=(204.8, 51.2), counts=(256, 64))
+    assert a.time == TimeConfig(theta=0.5, dt=0.002, t_final=10.0, startup_dt=0.002)
+
+
+def test_timescales_mirror_reference():
+    from paper_2006_16764_b200 import AlloyKernel, FreeGrowthKernel
+    from paper_2006_16764_b200.stepping import timescales
+
+    fg = timescales(FreeGrowthKernel().scales(), 0.03, 2.25e-4, dim=2).as_dict()
+    assert fg["dt_heat"] == 0.03 * 0.03 / (4.0 * 4.0) and fg["dt_solute"] == float("inf")
+    al = timescales(AlloyKernel().scales(), 0.8, 0.002, dim=2).as_dict()
+    p = AlloyKernel().params
+    assert al["kappa"] == 2.0 * 0.002 * p.solute_d0 / (0.8 * 0.8)
+
+
+def test_element_node_weights_sum_to_element_volume():
+    from paper_2006_16764_b200 import build_mesh
+    from paper_2006_16764_b200.driver import element_node_weights
+
+    for dim, ext, cnt in [(2, (0.96, 0.96), (32, 32)), (3, (0.48, 0.36, 0.24), (8, 6, 4))]:
+        m = build_mesh(dim, ext, cnt)
+        w = element_node_weights(m)
+        assert w.shape == (2 ** dim,)
+        assert abs(w.sum() - np.prod(m.spacing)) <= 1e-15 * np.prod(m.spacing) * 8

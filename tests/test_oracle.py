@@ -121,3 +121,42 @@ def test_oracle_time_steps_fg3d():
         prev, state = state, u
     assert newton == m["newton"] and gm == m["gmres"]
     assert rel(state, golden("run_fg3d_16_3")["state"]) <= 1e-8
+
+
+DIAG_CASES = sorted(k[len("diag_"):] for k in META if k.startswith("diag_") and k != "diag_tips_150")
+
+
+@pytest.mark.parametrize("case", DIAG_CASES)
+def test_oracle_step_diagnostics(case):
+    """Balance integrals, total solute and tip (driver.py:76-98,
+    diagnostics.py:69-89) against the reference on the seeded states."""
+    m = META["residual_" + case]
+    d = META["diag_" + case]
+    g = golden("residual_" + case)
+    spacing = [e / c for e, c in zip(m["extents"], m["counts"])]
+    st, sn, so = O.balance_integrals(m["counts"], spacing, g["new"], g["old"], g["prev"])
+    assert st == pytest.approx(d["w_dT"], rel=1e-13, abs=1e-17)
+    assert sn == pytest.approx(d["w_dphi_new"], rel=1e-13, abs=1e-17)
+    assert so == pytest.approx(d["w_dphi_old"], rel=1e-13, abs=1e-17)
+    if "total_solute" in d:
+        p = _params(m["model"], m.get("normalized", True))
+        assert O.total_solute(m["counts"], spacing, g["new"], p.composition, p.partition) == \
+            pytest.approx(d["total_solute"], rel=1e-13)
+    if "x_tip" in d:
+        n = g["new"].size // 2
+        level = 0.5 if m["model"] == "free_growth" else 0.0
+        tip, found = O.extract_tip(g["new"][: m["counts"][0] + 1], m["extents"][0], level)
+        assert (tip, found) == (d["x_tip"], d["found"])
+        assert n > 0
+
+
+def test_oracle_tip_profiles():
+    xs = np.linspace(0.0, 4.5, 151)
+    prof = {
+        "step": np.where(xs < 1.234, 1.0, 0.0),
+        "tanh": 0.5 * (1.0 - np.tanh((xs - 2.71) / 0.1)),
+        "none": np.ones_like(xs),
+        "exact": np.where(xs < 1.5, 1.0, np.where(np.isclose(xs, 1.5), 0.5, 0.0)),
+    }
+    for name, want in META["diag_tips_150"].items():
+        assert O.extract_tip(prof[name], 4.5, 0.5) == (want["x_tip"], want["found"]), name
