@@ -237,6 +237,25 @@ typedef struct uc_diag_args {
 int uc_step_diagnostics(uc_ctx* ctx, const double* unew, const double* old,
                         const double* prev, const uc_diag_args* args, double* out);
 
+/* map_u_to_c (alloy.py:119-127) of an owned block state into out[nloc] on the
+ * device (numpy's operation order, no contraction). */
+int uc_map_u_to_c(uc_ctx* ctx, const double* state, double composition, double* out);
+
+/* Snapshot / mesh text writers (vtkio.py:31-86), host side:
+ * byte-identical to the reference's files (numbers as Python repr prints
+ * them).  counts/extents describe the mesh (dim entries); fields are HOST
+ * arrays of n_nodes doubles in node order; format 0 = CSV
+ * (write_snapshot_csv), 1 = legacy VTK structured grid (write_snapshot_vtk,
+ * `comment` is its title line, "" = default).  `threads` host threads format
+ * rows.  No GPU needed. */
+int uc_write_snapshot(const char* path, int format, int dim, const int64_t* counts,
+                      const double* extents, int nfields, const char* const* names,
+                      const double* const* fields, const char* comment, int threads);
+int uc_write_mesh_vtk(const char* path, int dim, const int64_t* counts, const double* extents,
+                      int threads);
+/* repr(float(x)) as a NUL-terminated string (out needs 32 bytes) */
+int uc_repr_double(double x, char* out32);
+
 /* FP64 issue-rate probe (DFMA chains over all SMs), for the FP64 roofline
  * denominator; synchronises.  Not part of the reference interface. */
 int uc_fp64_probe(uc_ctx* ctx, int iters, double* ms_out, double* dfma_per_s);

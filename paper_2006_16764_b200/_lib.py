@@ -90,6 +90,11 @@ SIGNATURES = {
     "uc_fp64_probe": (_I, [_P, _I, C.POINTER(_D), C.POINTER(_D)]),
     "uc_initial_state": (_I, [_P, _I, C.POINTER(_D), C.POINTER(_D), _P]),
     "uc_step_diagnostics": (_I, [_P, _P, _P, _P, C.POINTER(DiagArgs), _P]),
+    "uc_map_u_to_c": (_I, [_P, _P, _D, _P]),
+    "uc_write_snapshot": (_I, [C.c_char_p, _I, _I, C.POINTER(_I64), C.POINTER(_D), _I,
+                               C.POINTER(C.c_char_p), C.POINTER(_P), C.c_char_p, _I]),
+    "uc_write_mesh_vtk": (_I, [C.c_char_p, _I, C.POINTER(_I64), C.POINTER(_D), _I]),
+    "uc_repr_double": (_I, [_D, C.c_char_p]),
     "uc_nccl_unique_id": (_I, [C.c_char_p, _P]),
     "uc_comm_init_nccl": (_I, [C.c_char_p, _P, _I, _I]),
     "uc_comm_finalize": (_I, []),

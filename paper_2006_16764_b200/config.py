@@ -1,15 +1,14 @@
-"""Run configuration dataclasses (mirrors undercool/config.py:27-117,224-232).
+"""Run configuration (mirrors undercool/config.py:27-117,150-174,224-232).
 
-Only the in-memory configuration that ``driver.simulate`` reads is mirrored:
-the sections, their defaults, ``validate`` and ``default_config``.  The text
-file round trip (``load_config`` / ``save_config`` / ``parse_overrides``) and
-the output section's file writing belong to the reference's control plane
-and are out of scope.  ``simulate`` also accepts the
-reference's own ``RunConfig`` objects (attribute access only).
+The sections and defaults, ``validate``, ``default_config`` and
+``save_config`` (the ``config.used`` file ``driver.run`` writes, byte-identical
+to the reference's).  ``driver.simulate`` also accepts the reference's own
+``RunConfig`` objects (attribute access only).
 """
 
 from __future__ import annotations
 
+import dataclasses
 from dataclasses import dataclass, field
 
 from .errors import ConfigError
@@ -17,7 +16,7 @@ from .models import AlloyKernel, AlloyParams, FreeGrowthKernel, FreeGrowthParams
 from .newton import NewtonConfig
 from .precond import PrecondConfig
 
-__all__ = ["MeshConfig", "TimeConfig", "OutputConfig", "RunConfig", "default_config"]
+__all__ = ["MeshConfig", "TimeConfig", "OutputConfig", "RunConfig", "save_config", "default_config"]
 
 
 @dataclass
@@ -94,6 +93,46 @@ class RunConfig:
         if self.model == "free_growth":
             return FreeGrowthKernel(self.free_growth)
         return AlloyKernel(self.alloy)
+
+
+_RUN_KEYS = ("model", "seed", "perturbation", "smooth_interface", "retry_halve_dt")
+_DATACLASS_SECTIONS = ("mesh", "time", "solver", "precond", "output", "free_growth", "alloy")
+
+
+def _text(v) -> str:
+    """One value as config.py:120-127 prints it (repr for floats, true/false,
+    comma-separated sequences)."""
+    if v is True or v is False:
+        return "true" if v else "false"
+    if isinstance(v, (tuple, list)):
+        return ", ".join(map(repr, v))
+    return repr(v) if isinstance(v, float) else str(v)
+
+
+def save_config(cfg, path=None) -> str:
+    """The ``config.used`` text of config.py:150-174: [run], one section per
+    dataclass (Newton without its nested gmres), then [gmres]; the layout
+    configparser writes ("key = value" lines, a blank line after each
+    section).  Reading config files back (load_config / parse_overrides) is
+    the reference CLI's business and is not mirrored."""
+    sections = [("run", [(k, getattr(cfg, k)) for k in _RUN_KEYS])]
+    for name in _DATACLASS_SECTIONS:
+        sub = getattr(cfg, name)
+        if dataclasses.is_dataclass(sub):
+            sections.append((name, [(f.name, getattr(sub, f.name)) for f in dataclasses.fields(sub)
+                                    if f.name != "gmres"]))
+    g = cfg.solver.gmres
+    sections.append(("gmres", [(f.name, getattr(g, f.name)) for f in dataclasses.fields(g)]))
+    lines = []
+    for name, items in sections:
+        lines.append(f"[{name}]")
+        lines.extend(f"{k} = {_text(v)}" for k, v in items)
+        lines.append("")
+    text = "\n".join(lines) + "\n"
+    if path is not None:
+        with open(path, "w") as fh:
+            fh.write(text)
+    return text
 
 
 def default_config(model: str) -> RunConfig:

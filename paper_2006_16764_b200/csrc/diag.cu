@@ -234,6 +234,16 @@ __global__ void __launch_bounds__(1024) k_diag_tip(const DiagArgs a) {
   a.out[D_FOUND] = found;
 }
 
+// map_u_to_c (alloy.py:119-127): composition / (2k) * (1 + k - (1 - k) phi) * (1 + (1 - k) u)
+__global__ void k_composition(int64_t n, const double* __restrict__ st, double c2k, double k,
+                              double* __restrict__ out) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  const double omk = 1.0 - k, opk = 1.0 + k;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride)
+    out[i] = __dmul_rn(__dmul_rn(c2k, __dsub_rn(opk, __dmul_rn(omk, st[i]))),
+                       __dadd_rn(1.0, __dmul_rn(omk, st[n + i])));
+}
+
 static unsigned diag_grid(int64_t n) {
   int64_t b = (n + UC_DIAG_THREADS * 8 - 1) / (UC_DIAG_THREADS * 8);
   if (b < 1) b = 1;
@@ -296,6 +306,18 @@ extern "C" int uc_step_diagnostics(uc_ctx* c, const double* unew, const double* 
   if ((args->what & UC_DIAG_SOLUTE) && c->grid.hi < c->grid.nslow)
     return set_error(UC_ERR_ARG, "uc_step_diagnostics: slab needs the group entry point (ghost plane)");
   return step_diagnostics(c, unew, old, prev, args, out);
+}
+
+extern "C" int uc_map_u_to_c(uc_ctx* c, const double* state, double composition, double* out) {
+  if (!c || !state || !out) return set_error(UC_ERR_ARG, "uc_map_u_to_c: bad argument");
+  const int64_t n = c->grid.nloc;
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > (int64_t)c->num_sms * 16) blocks = (int64_t)c->num_sms * 16;
+  if (blocks < 1) blocks = 1;
+  k_composition<<<(unsigned)blocks, 256, 0, c->stream>>>(n, state, composition / (2.0 * c->params.kpart),
+                                                         c->params.kpart, out);
+  UC_CUDA_OK(cudaGetLastError());
+  return UC_OK;
 }
 
 extern "C" int uc_step_diagnostics_group(uc_ctx* const* ctxs, int n, const double* const* unew,

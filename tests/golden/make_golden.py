@@ -353,12 +353,79 @@ def diag_cases(meta):
     meta["diag_tips_150"] = tips
 
 
+def writer_cases(meta):
+    """Reference writer outputs (vtkio.py:31-86, driver.py:244-275, config.py:150-174)
+    on golden states, gzipped under tests/golden/writers/."""
+    import gzip
+    import tempfile
+
+    from undercool.config import save_config
+    from undercool.driver import _field_dict, run
+    from undercool.vtkio import write_mesh_vtk, write_snapshot_csv, write_snapshot_vtk
+
+    wdir = os.path.join(OUT, "writers")
+    os.makedirs(wdir, exist_ok=True)
+
+    def keep(src, name):
+        with open(src, "rb") as fh, open(os.path.join(wdir, name + ".gz"), "wb") as out:
+            out.write(gzip.compress(fh.read(), mtime=0))
+
+    cases = [("fg2d_32_10", "free_growth", 2, (0.96, 0.96), (32, 32), 1e-4),
+             ("al2d_128x32_10", "alloy", 2, (102.4, 25.6), (128, 32), 0.02),
+             ("fg3d_16_3", "free_growth", 3, (0.48, 0.48, 0.48), (16, 16, 16), 6.75e-4)]
+    info = {}
+    with tempfile.TemporaryDirectory() as tmp:
+        for name, model, dim, ext, cnt, t in cases:
+            cfg = default_config(model)
+            mesh = uc.build_mesh(dim, ext, cnt)
+            k = cfg.kernel()
+            state = np.load(os.path.join(OUT, f"driver_{name}.npz"))["state"]
+            fields = _field_dict(cfg, k, state)
+            write_snapshot_csv(mesh, fields, os.path.join(tmp, "s.csv"))
+            write_snapshot_vtk(mesh, fields, os.path.join(tmp, "s.vtk"), comment=f"t = {t!r}")
+            keep(os.path.join(tmp, "s.csv"), f"snapshot_{name}.csv")
+            keep(os.path.join(tmp, "s.vtk"), f"snapshot_{name}.vtk")
+            info[name] = dict(model=model, dim=dim, extents=ext, counts=cnt, t=t,
+                              fields=list(fields))
+            if "composition" in fields:
+                np.savez_compressed(os.path.join(wdir, f"composition_{name}.npz"),
+                                    composition=fields["composition"])
+        for name, dim, ext, cnt in [("mesh2d_6x4", 2, (0.6, 0.4), (6, 4)),
+                                    ("mesh3d_4x3x2", 3, (0.4, 0.3, 0.2), (4, 3, 2))]:
+            write_mesh_vtk(uc.build_mesh(dim, ext, cnt), os.path.join(tmp, "m.vtk"))
+            keep(os.path.join(tmp, "m.vtk"), name + ".vtk")
+            info[name] = dict(dim=dim, extents=ext, counts=cnt)
+        for model in ("free_growth", "alloy"):
+            with open(os.path.join(tmp, "c.txt"), "w") as fh:
+                fh.write(save_config(default_config(model)))
+            keep(os.path.join(tmp, "c.txt"), f"config_{model}.used")
+        # a full run() of tests/test_driver.py:22-27 with snapshots every 5 steps
+        cfg = _small_fg()
+        cfg.output.directory = os.path.join(tmp, "run")
+        cfg.output.snapshot_every = 5
+        code, _ = run(cfg)
+        names = sorted(os.listdir(cfg.output.directory))
+        keep(os.path.join(cfg.output.directory, "runlog.csv"), "run_fg2d_32_10.runlog.csv")
+        with open(os.path.join(cfg.output.directory, "summary.json")) as fh:
+            summ = json.load(fh)
+        info["run_fg2d_32_10"] = dict(code=code, files=names, summary_keys=sorted(summ),
+                                      snapshots=summ["snapshots"])
+    meta["writers"] = info
+
+
 def main():
     meta = {"generator": "tests/golden/make_golden.py", "reference": REF}
+    if "--only-writers" in sys.argv:
+        meta = json.load(open(os.path.join(OUT, "golden.json")))
+        writer_cases(meta)
+        with open(os.path.join(OUT, "golden.json"), "w") as fh:
+            json.dump(meta, fh, indent=1, sort_keys=True)
+        return
     if "--only-driver" in sys.argv:
         meta = json.load(open(os.path.join(OUT, "golden.json")))
         driver_cases(meta)
         diag_cases(meta)
+        writer_cases(meta)
         with open(os.path.join(OUT, "golden.json"), "w") as fh:
             json.dump(meta, fh, indent=1, sort_keys=True)
         return
@@ -375,6 +442,7 @@ def main():
         run_cases(meta)
         driver_cases(meta)
         diag_cases(meta)
+        writer_cases(meta)
     else:
         meta.update({k: v for k, v in old.items() if k.startswith("run_")})
     # measured with the reference in SURVEY.md section 8(c) (453 s on this host):

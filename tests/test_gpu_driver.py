@@ -150,3 +150,75 @@ def test_simulate_matches_reference_records(uc, case):
     if g["status"] == "ok":
         assert rel(res.state, golden("driver_" + case)["state"]) <= 1e-8
         assert res.device_state.is_cuda
+
+
+def test_composition_map_bit_exact(uc):
+    import os
+
+    import torch
+
+    from conftest import GOLDEN
+    from paper_2006_16764_b200 import _lib as L
+    from paper_2006_16764_b200 import device as D
+
+    m = META["writers"]["al2d_128x32_10"]
+    mesh = uc.build_mesh(m["dim"], m["extents"], m["counts"])
+    k = uc.AlloyKernel()
+    st = torch.tensor(golden("driver_al2d_128x32_10")["state"], device="cuda")
+    out = torch.empty(mesh.n_nodes, dtype=torch.float64, device="cuda")
+    ctx = D.context_for(mesh, k)
+    L.check(ctx.lib.uc_map_u_to_c(ctx.bind(), L.ptr(st), k.params.composition, L.ptr(out)))
+    want = np.load(os.path.join(GOLDEN, "writers", "composition_al2d_128x32_10.npz"))["composition"]
+    assert np.array_equal(out.cpu().numpy(), want)
+
+
+def test_run_artifacts_match_reference_layout_and_are_deterministic(uc, tmp_path):
+    """tests/test_driver.py:73-115 on the device path: same files, summary keys
+    and snapshot registry as the reference's run(); two runs byte-identical."""
+    import gzip
+    import json
+    import os
+
+    from conftest import GOLDEN
+    from paper_2006_16764_b200.config import MeshConfig, OutputConfig, RunConfig, TimeConfig
+    from paper_2006_16764_b200.driver import run
+
+    want = META["writers"]["run_fg2d_32_10"]
+    outs = []
+    for name in ("a", "b"):
+        cfg = RunConfig()
+        cfg.mesh = MeshConfig(dimension=2, extents=(0.96, 0.96), counts=(32, 32))
+        cfg.time = TimeConfig(theta=0.5, dt=1e-5, t_final=1e-4)
+        cfg.output = OutputConfig(directory=str(tmp_path / name), snapshot_every=5)
+        code, res = run(cfg)
+        assert code == want["code"] == 0
+        d = cfg.output.directory
+        assert sorted(os.listdir(d)) == want["files"]
+        summ = json.load(open(os.path.join(d, "summary.json")))
+        assert sorted(summ) == want["summary_keys"]
+        assert summ["snapshots"] == want["snapshots"]
+        assert summ["status"] == "ok" and summ["steps"] == 10
+        outs.append({f: open(os.path.join(d, f), "rb").read()
+                     for f in want["files"] if f != "summary.json"})
+    cfg_a = outs[0].pop("config.used")
+    outs[1].pop("config.used")  # differs only in output.directory
+    assert outs[0] == outs[1]
+    mine = outs[0]["runlog.csv"].decode().splitlines()
+    with open(os.path.join(GOLDEN, "writers", "run_fg2d_32_10.runlog.csv.gz"), "rb") as fh:
+        ref = gzip.decompress(fh.read()).decode().splitlines()
+    assert len(mine) == len(ref)
+    nhead = sum(1 for line in ref if line.startswith("#")) + 1
+    assert mine[:nhead] == ref[:nhead]  # timescales, theta, dt, column names
+    for a, b in zip(mine[nhead:], ref[nhead:]):
+        ca, cb = a.split(","), b.split(",")
+        assert ca[:5] == cb[:5]  # step, time, newton, gmres, lambda history
+        for x, y in zip(ca[5:], cb[5:]):
+            # the reference's numpy-2 scalars print as np.float64(...)
+            y = y.removeprefix("np.float64(").removesuffix(")")
+            assert float(x) == pytest.approx(float(y), rel=1e-3, abs=1e-12)
+    assert cfg_a == gzip.decompress(
+        open(os.path.join(GOLDEN, "writers", "config_free_growth.used.gz"), "rb").read()).replace(
+        b"dimension = 2\nextents = 4.5, 4.5\ncounts = 150, 150",
+        b"dimension = 2\nextents = 0.96, 0.96\ncounts = 32, 32").replace(
+        b"dt = 0.000225\nt_final = 0.14", b"dt = 1e-05\nt_final = 0.0001").replace(
+        b"directory = out\nsnapshot_every = 0", f"directory = {tmp_path / 'a'}\nsnapshot_every = 5".encode())

@@ -142,3 +142,15 @@ def test_element_node_weights_sum_to_element_volume():
         w = element_node_weights(m)
         assert w.shape == (2 ** dim,)
         assert abs(w.sum() - np.prod(m.spacing)) <= 1e-15 * np.prod(m.spacing) * 8
+
+
+def test_run_config_error_exit_code(tmp_path):
+    """tests/test_driver.py:156-160: a bad config returns EXIT_CONFIG before any device work."""
+    from paper_2006_16764_b200.config import RunConfig
+    from paper_2006_16764_b200.driver import EXIT_CONFIG, run
+
+    cfg = RunConfig()
+    cfg.time.dt = -1.0
+    cfg.output.directory = str(tmp_path / "out")
+    code, res = run(cfg)
+    assert code == EXIT_CONFIG and res.status == "config_error"
