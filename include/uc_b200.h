@@ -94,6 +94,7 @@ typedef struct uc_scheme {
 /* PrecondConfig (undercool/precond.py:54-71). */
 #define UC_ORDER_MULTICOLOR 0
 #define UC_ORDER_LEXICOGRAPHIC 1
+#define UC_ORDER_LEXICOGRAPHIC_WAVEFRONT 2  /* same sweep, grid-barrier wavefront kernel (validation) */
 typedef struct uc_precond_cfg {
   int32_t kind;           /* UC_PC_* */
   int32_t sweeps;

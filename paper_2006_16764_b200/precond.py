@@ -19,6 +19,7 @@ one.  kind="direct" (SuperLU) has no device implementation and raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import weakref
 from dataclasses import dataclass
 
@@ -173,6 +174,8 @@ def build_precond(mesh, kernel, state, scheme, config: PrecondConfig | None = No
     pc.kind = _KINDS[cfg.kind]
     pc.sweeps, pc.cycles, pc.levels, pc.coarse_sweeps = cfg.sweeps, cfg.cycles, cfg.levels, cfg.coarse_sweeps
     pc.ordering = 1 if cfg.ordering == "lexicographic" else 0
+    if pc.ordering == 1 and os.environ.get("UC_LEX_WAVEFRONT") == "1":
+        pc.ordering = 2  # the same sweep on the grid-barrier wavefront kernel (validation)
     sc = scheme_struct(scheme)
     rc = ctx.lib.uc_precond_build(ctx.bind(), C.byref(sc), L.ptr(st), C.byref(pc))
     if rc == L.UC_ERR_ARG:

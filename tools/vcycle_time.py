@@ -17,6 +17,7 @@ from paper_2006_16764_b200.models import seed_initial_condition  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--counts", type=int, nargs="+", default=[2048, 2048])
 ap.add_argument("--reps", type=int, default=20)
+ap.add_argument("--ordering", default="multicolor")
 a = ap.parse_args()
 mesh = uc.build_mesh(len(a.counts), [0.03 * c for c in a.counts], a.counts)
 k = uc.FreeGrowthKernel()
@@ -27,7 +28,7 @@ for rep in range(3):
     pc = None  # recycle the previous hierarchy (buffers + captured graph)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    pc = uc.build_precond(mesh, k, u0, sc, uc.PrecondConfig(ordering="multicolor"))
+    pc = uc.build_precond(mesh, k, u0, sc, uc.PrecondConfig(ordering=a.ordering))
     torch.cuda.synchronize()
     t1 = time.perf_counter()
     v = torch.randn_like(u0)
