@@ -192,9 +192,17 @@ def vcycle_bytes(pc, N, dim):
     """Algorithmic HBM bytes of one BlockPrecond.apply (both blocks), counting
     stencil + vector streams once per pass (x neighbours cached)."""
     K = 3 ** dim
+    C = 2 ** dim  # colours
     cfg = pc.cfg
     rows = [int(np.prod(s)) for s in pc.level_shapes]
-    sweep = lambda R: (8 * K + 24) * R  # noqa: E731  one half-sweep: A rows, b, x r/w
+
+    def smooth(R, sweeps):
+        # colour passes actually executed: 2 C per symmetric sweep, minus the
+        # repeated colour folded at every turn (DESIGN.md section 8); each
+        # pass streams its colour's stencil rows, b and x once
+        passes = 2 * C * sweeps - (2 * sweeps - 1) if sweeps > 0 else 0
+        return passes / C * (8 * K + 24) * R
+
     total = 0.0
 
     def cyc(l):
@@ -202,9 +210,9 @@ def vcycle_bytes(pc, N, dim):
         R = rows[l]
         total += 8 * R  # zero x
         if l == len(rows) - 1:
-            total += 2 * cfg.coarse_sweeps * sweep(R)
+            total += smooth(R, cfg.coarse_sweeps)
             return
-        total += 4 * cfg.sweeps * sweep(R) / 2 * 2  # pre + post, forward + reverse
+        total += 2 * smooth(R, cfg.sweeps)  # pre + post
         total += (8 * K + 24) * R  # residual
         total += 8 * R + 8 * rows[l + 1]  # restrict
         cyc(l + 1)
@@ -293,6 +301,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="fg2d_2048", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-lex", action="store_true", help="skip the lexicographic-ordering Newton solve")
     ap.add_argument("--no-newton", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -401,8 +410,17 @@ def main():
 
     res_bytes = 32 * Dof
     achieved = res_bytes / (t_res * 1e-3) / 1e9
+    # DRAM bytes per launch of this kernel from the committed ncu --set full
+    # capture (profiles/r01/ncu_traffic.json), when it covers this workload
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")) as fh:
+            traffic = json.load(fh)["kernels"].get(roofline_kernel_name(w), {}).get(args.workload)
+    except (OSError, ValueError, KeyError):
+        traffic = None
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(achieved / hbm_peak, 4), "traffic": None,
+                "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
+                "algorithmic_bytes": res_bytes,
                 "kernel": f"k_residual<{w['dim']},{'FG' if w['model'] == 'free_growth' else 'ALLOY'},NEW>",
                 "bytes_per_dof": 32, "ms_per_launch": round(t_res, 4), "peak_source": peak_src,
                 "note": "fp64-issue-bound kernel; HBM fraction ceiling ~20-30% in 2D (DESIGN.md)"}
@@ -543,7 +561,25 @@ def main():
                       "vcycle_apply_ms": round(t_apply, 3),
                       "vcycle_gbs": round(vb / (t_apply * 1e-3) / 1e9, 1),
                       "vcycle_hbm_frac": round(vb / (t_apply * 1e-3) / 1e9 / hbm_peak, 4),
-                      "case": "seed IC, step 0 (backward-Euler startup), default solver settings"}
+                      "case": "seed IC, step 0 (backward-Euler startup), default solver settings",
+                      "ordering": "multicolor"}
+            # the reference's DEFAULT smoother ordering: exact sequential
+            # (lexicographic) Gauss-Seidel, pipelined wavefront kernel
+            if not args.no_lex and N <= 2049 * 2049:
+                pc = uc.build_precond(mesh, kern, st, sc0, uc.PrecondConfig(ordering="lexicographic"))
+                r0 = uc.TimestepResidual(mesh, kern, st, st, sc0)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                _, rep_l = uc.newton_solve(r0, st, uc.NewtonConfig(), precond_apply=pc.apply)
+                torch.cuda.synchronize()
+                t_lex = time.perf_counter() - t0
+                t_apply_l = timed(lambda: pc.device_apply(vv, check=False), 3)
+                pc = r0 = None
+                newton["lexicographic"] = {
+                    "sec_per_newton_iteration": round(t_lex / max(rep_l.iterations, 1), 5),
+                    "newton_iterations": rep_l.iterations, "gmres_per_newton": rep_l.gmres_iterations,
+                    "vcycle_apply_ms": round(t_apply_l, 3),
+                    "note": "reference default ordering; sequential sweep as a pipelined wavefront (fronts i+2j)"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
