@@ -469,14 +469,23 @@ def main():
     ev_in = [torch.cuda.Event() for _ in range(2)]
     ev_out = [torch.cuda.Event() for _ in range(2)]
 
+    def upload(i):
+        k = i % 2
+        with torch.cuda.stream(s_in):
+            s_in.wait_event(ev_out[k])  # buffer k free again (step i-2's results left)
+            u_d[k].copy_(u_pin, non_blocking=True)
+            v_d[k].copy_(v_pin, non_blocking=True)
+            ev_in[k].record(s_in)
+
     def e2e_run(nsteps):
+        # the upload of step i+1 is enqueued before step i's API calls (which
+        # synchronise on their non-finite checks), so it overlaps step i's
+        # compute and step i-1's download
+        upload(0)
         for i in range(nsteps):
             k = i % 2
-            with torch.cuda.stream(s_in):
-                s_in.wait_event(ev_out[k])  # buffer k free again (its results left)
-                u_d[k].copy_(u_pin, non_blocking=True)
-                v_d[k].copy_(v_pin, non_blocking=True)
-                ev_in[k].record(s_in)
+            if i + 1 < nsteps:
+                upload(i + 1)
             stream.wait_event(ev_in[k])
             F = res(u_d[k])
             Jv = uc.jfnk_matvec(res, u_d[k], F, v_d[k])
@@ -486,6 +495,8 @@ def main():
                 f_pin[k].copy_(F, non_blocking=True)
                 j_pin[k].copy_(Jv, non_blocking=True)
                 ev_out[k].record(s_out)
+            F.record_stream(s_out)  # keep F, Jv alive until their download ran
+            Jv.record_stream(s_out)
 
     e2e_run(args.warmup)
     torch.cuda.synchronize()
