@@ -196,24 +196,28 @@ def vcycle_bytes(pc, N, dim):
     cfg = pc.cfg
     rows = [int(np.prod(s)) for s in pc.level_shapes]
 
-    def smooth(R, sweeps):
+    def smooth(R, sweeps, srow):
         # colour passes actually executed: 2 C per symmetric sweep, minus the
         # repeated colour folded at every turn; each
         # pass streams its colour's stencil rows, b and x once
         passes = 2 * C * sweeps - (2 * sweeps - 1) if sweeps > 0 else 0
-        return passes / C * (8 * K + 24) * R
+        return passes / C * (srow + 24) * R
 
     total = 0.0
+
+    # stencil rows of uniform tiles are not read (one shared row per level)
+    stencil = [8 * K * (1.0 - 0.5 * (pc.uniform_fraction(l, 0) + pc.uniform_fraction(l, 1)))
+               for l in range(len(rows))]
 
     def cyc(l):
         nonlocal total
         R = rows[l]
         total += 8 * R  # zero x
         if l == len(rows) - 1:
-            total += smooth(R, cfg.coarse_sweeps)
+            total += smooth(R, cfg.coarse_sweeps, stencil[l])
             return
-        total += 2 * smooth(R, cfg.sweeps)  # pre + post
-        total += (8 * K + 24) * R  # residual
+        total += 2 * smooth(R, cfg.sweeps, stencil[l])  # pre + post
+        total += (stencil[l] + 24) * R  # residual
         total += 8 * R + 8 * rows[l + 1]  # restrict
         cyc(l + 1)
         total += 8 * rows[l + 1] + 16 * R  # prolong-add
@@ -221,7 +225,7 @@ def vcycle_bytes(pc, N, dim):
     for c in range(cfg.cycles):
         cyc(0)
         if c > 0:
-            total += (8 * K + 24) * rows[0] + 24 * rows[0]  # residual + x += e
+            total += (stencil[0] + 24) * rows[0] + 24 * rows[0]  # residual + x += e
     return 2 * total  # both field blocks
 
 

@@ -86,6 +86,7 @@ SIGNATURES = {
     "uc_precond_apply": (_I, [_P, _P, _P]),
     "uc_precond_stencil": (_I, [_P, _I, _I, _P]),
     "uc_precond_levels": (_I, [_P, C.POINTER(_I64)]),
+    "uc_precond_uniform": (_I, [_P, _I, _I, C.POINTER(_D)]),
     "uc_status": (_I, [_P, C.POINTER(Status), _I]),
     "uc_fp64_probe": (_I, [_P, _I, C.POINTER(_D), C.POINTER(_D)]),
     "uc_initial_state": (_I, [_P, _I, C.POINTER(_D), C.POINTER(_D), _P]),

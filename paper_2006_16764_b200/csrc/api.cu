@@ -284,6 +284,11 @@ int uc_precond_stencil(uc_ctx* c, int level, int block, double* host_out) {
   return precond_stencil(c, level, block, host_out);
 }
 
+int uc_precond_uniform(uc_ctx* c, int level, int block, double* frac) {
+  if (!c || !frac) return set_error(UC_ERR_ARG, "uc_precond_uniform: NULL argument");
+  return precond_uniform_fraction(c, level, block, frac);
+}
+
 int uc_precond_levels(uc_ctx* c, int64_t* shapes) {
   if (!c) return set_error(UC_ERR_ARG, "uc_precond_levels: NULL argument");
   return precond_levels(c, shapes);

@@ -105,5 +105,6 @@ int precond_apply_group(const Group& G, const double* const* v, double* const* o
 int precond_apply(uc_ctx* c, const double* v, double* out);
 int precond_stencil(uc_ctx* c, int level, int block, double* host_out);
 int precond_levels(uc_ctx* c, int64_t* shapes);
+int precond_uniform_fraction(uc_ctx* c, int level, int block, double* frac);
 void precond_destroy(Precond* p);
 }  // namespace uc

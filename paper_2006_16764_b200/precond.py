@@ -135,6 +135,13 @@ class BlockPrecond:
                 "uc_precond_stencil")
         return out
 
+    def uniform_fraction(self, level: int, block: int) -> float:
+        """Share of stencil tiles the apply kernels read from one shared row."""
+        out = C.c_double()
+        L.check(self._ctx.lib.uc_precond_uniform(self._ctx.bind(), level, block, C.byref(out)),
+                "uc_precond_uniform")
+        return out.value
+
     def level_matrix(self, level: int, block: int):
         return _stencil_to_csr(self.level_stencil(level, block), self.level_shapes[level], self.dim)
 
