@@ -51,3 +51,33 @@ def test_pipelined_lexicographic_is_bitwise_the_sequential_sweep(dim, counts, mo
         a = _apply(uc, mesh, k, st, v, False, kind)
         b = _apply(uc, mesh, k, st, v, True, kind)
         assert torch.equal(a, b), (kind, float((a - b).abs().max()))
+
+
+@pytest.mark.parametrize("dim,counts,model", [(2, (64, 40), "free_growth"), (2, (33, 95), "alloy"),
+                                              (3, (16, 16, 16), "free_growth"), (3, (12, 10, 8), "alloy")])
+def test_uniform_tiles_are_bitwise_the_explicit_stencils(dim, counts, model):
+    """Apply kernels read one shared row for tiles whose 32 stencil rows are
+    bitwise equal to it (csrc/precond.cu k_tile_uniform); the result must be
+    identical to reading every row (UC_PC_NO_UNIFORM=1)."""
+    import paper_2006_16764_b200 as uc
+
+    mesh = uc.build_mesh(dim, [0.03 * c for c in counts], counts)
+    k = uc.FreeGrowthKernel() if model == "free_growth" else uc.AlloyKernel()
+    st = uc.models.seed_initial_condition_device(mesh, uc.FreeGrowthParams()) if model == "free_growth" \
+        else uc.models.directional_initial_condition_device(mesh, uc.AlloyParams(), amplitude=0.5, smooth=True)
+    v = torch.randn_like(st)
+    outs = []
+    for flag in ("0", "1"):
+        if flag == "1":
+            os.environ["UC_PC_NO_UNIFORM"] = "1"
+        try:
+            for ordering in ("multicolor", "lexicographic"):
+                pc = uc.build_precond(mesh, k, st, uc.ThetaScheme(0.5, 2.25e-4, 1),
+                                      uc.PrecondConfig(ordering=ordering))
+                if flag == "0" and ordering == "multicolor" and model == "free_growth":
+                    assert pc.uniform_fraction(0, 1) > 0.5  # constant-coefficient heat block
+                outs.append(pc.apply(v).clone())
+                pc = None
+        finally:
+            os.environ.pop("UC_PC_NO_UNIFORM", None)
+    assert torch.equal(outs[0], outs[2]) and torch.equal(outs[1], outs[3])
