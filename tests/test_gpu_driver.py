@@ -222,3 +222,25 @@ def test_run_artifacts_match_reference_layout_and_are_deterministic(uc, tmp_path
         b"dimension = 2\nextents = 0.96, 0.96\ncounts = 32, 32").replace(
         b"dt = 0.000225\nt_final = 0.14", b"dt = 1e-05\nt_final = 0.0001").replace(
         b"directory = out\nsnapshot_every = 0", f"directory = {tmp_path / 'a'}\nsnapshot_every = 5".encode())
+
+
+def test_startup_substeps_run(uc):
+    """Startup interval cut into implicit substeps (driver.py:107-131, 190-194):
+    the reference itself crashes here, so check the
+    policy: two substeps of dt/2 at step 0 and 1, records at whole steps."""
+    from paper_2006_16764_b200.config import MeshConfig, TimeConfig, default_config
+    from paper_2006_16764_b200.driver import simulate
+
+    cfg = default_config("alloy")
+    cfg.mesh = MeshConfig(dimension=2, extents=(102.4, 25.6), counts=(128, 32))
+    cfg.time = TimeConfig(theta=0.5, dt=0.002, t_final=0.006, startup_dt=0.001)
+    res = simulate(cfg)
+    assert res.status == "ok" and res.steps_completed == 3
+    assert [r["time"] for r in res.records] == pytest.approx([0.002, 0.004, 0.006], rel=1e-15)
+    # the startup steps ran two Newton solves each (substeps), the last one one
+    assert all(r["newton_iters"] >= 2 for r in res.records[:2])
+    assert np.isfinite(res.state).all() and np.abs(res.state[: mesh_nodes(cfg)]).max() <= 1.0 + 1e-6
+
+
+def mesh_nodes(cfg):
+    return int(np.prod([c + 1 for c in cfg.mesh.counts]))
