@@ -121,6 +121,7 @@ int uc_ctx_destroy(uc_ctx* c) {
   if (c->flags_host) cudaFreeHost(c->flags_host);
   cudaFree(c->locate_key);
   cudaFree(c->diag_ws);
+  cudaFree(c->ebuf);
   for (int s = 0; s < 5; ++s)
     for (int d = 0; d < 2; ++d) cudaFree(c->ghost[s][d]);
   delete c;

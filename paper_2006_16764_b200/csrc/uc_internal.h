@@ -51,6 +51,8 @@ struct uc_ctx {
   unsigned int* flags_host = nullptr; // mapped pinned host memory
   unsigned long long* locate_key = nullptr;
   double* diag_ws = nullptr;      // diag.cu partials + ticket (lazy)
+  double* ebuf = nullptr;         // residual.cu: edge contributions of the ring-free 2D tiles (lazy)
+  size_t ebuf_n = 0;
   // ghost planes [slot][side] -> [2][plane]; slots 0 u, 1 old, 2 prev, 3 v, 4 state
   double* ghost[5][2] = {{nullptr, nullptr}, {nullptr, nullptr}, {nullptr, nullptr},
                          {nullptr, nullptr}, {nullptr, nullptr}};
