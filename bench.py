@@ -326,7 +326,7 @@ def run_slabs(args, w, rank, world, local, dist):
                        "dof": D_glob, "dof_per_step": 2 * D_glob,
                        "parallelism": f"slab x{world} (NCCL ghost planes + allreduce)",
                        "l2": "per-rank inputs larger than L2; no flush"},
-            "gpu_launches": 3 * args.steps, "clocks": clk.summary(), "roofline": None,
+            "gpu_launches": 5 * args.steps, "clocks": clk.summary(), "roofline": None,
             "e2e": e2e, "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)
@@ -550,7 +550,7 @@ def main():
     e2e = {"value": round(world * 2 * Dof / (e2e_ms * 1e-3) / 1e6, 2), "unit": "MDoF/s",
            "h2d_bytes_per_step": 2 * Dof * 8, "d2h_bytes_per_step": 2 * Dof * 8,
            "ms_per_step": round(e2e_ms, 3), "copies": "pinned, double-buffered copy streams"}
-    launches_per_step = 3  # residual tile, |v| reduction, Jv tile
+    launches_per_step = 5  # residual tile + edge fix-up, |v| reduction, Jv tile + edge fix-up
 
     # ---- Newton step on the seeded dendrite --------------------------
     # release the fill-phase working set first (512^3: ~2.2 GB per vector)
