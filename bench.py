@@ -229,36 +229,50 @@ def vcycle_bytes(pc, N, dim):
     return 2 * total  # both field blocks
 
 
-def run_slabs(args, w, rank, world, local, dist):
+def run_slabs(args, w, rank, world, local, dist, emulate=0):
     """N > 1: one slab per GPU of a weak-scaled mesh (counts[-1] x world), NCCL
-    ghost planes and allreduce inside the library (paper_2006_16764_b200.parallel)."""
+    ghost planes and allreduce inside the library (paper_2006_16764_b200.parallel).
+    emulate=K (testing, --emulate-slabs): the same code path with K slabs driven
+    by this one process on one GPU (planes copied on the stream instead of NCCL)."""
     import torch
 
     import paper_2006_16764_b200 as uc
     from paper_2006_16764_b200.parallel import SlabGroup, SlabResidual
 
     dev = torch.device("cuda", local)
+    nslab = emulate if emulate else world
     counts = list(w["counts"])
     extents = list(w["extents"])
-    counts[-1] *= world
-    extents[-1] *= world
+    counts[-1] *= nslab
+    extents[-1] *= nslab
     mesh = uc.build_mesh(w["dim"], extents, counts)
     kern = uc.FreeGrowthKernel() if w["model"] == "free_growth" else uc.AlloyKernel()
     sc = uc.ThetaScheme(w["theta"], w["dt"], w["step"])
-    grp = SlabGroup.from_torch_dist(mesh, kern)
-    lo, hi = grp.slabs[0]
-    nloc = (hi - lo) * grp.plane
+    grp = SlabGroup.local(mesh, kern, nslab) if emulate else SlabGroup.from_torch_dist(mesh, kern)
+    nlocs = [(hi - lo) * grp.plane for lo, hi in grp.slabs]
     rng = np.random.default_rng(11 + rank)
-    if w["model"] == "free_growth":
-        mk = lambda: np.concatenate([0.5 + 0.3 * rng.standard_normal(nloc), 1.0 + 0.2 * rng.standard_normal(nloc)])  # noqa: E731
-    else:
-        mk = lambda: np.concatenate([np.tanh(rng.standard_normal(nloc)), -0.5 + 0.4 * rng.standard_normal(nloc)])  # noqa: E731
+
+    def mk(nloc):
+        if w["model"] == "free_growth":
+            return np.concatenate([0.5 + 0.3 * rng.standard_normal(nloc), 1.0 + 0.2 * rng.standard_normal(nloc)])
+        return np.concatenate([np.tanh(rng.standard_normal(nloc)), -0.5 + 0.4 * rng.standard_normal(nloc)])
+
     sp = grp.space
-    u, old, prev = (sp.wrap([torch.from_numpy(mk()).to(dev)]) for _ in range(3))
-    v = sp.wrap([torch.from_numpy(np.random.default_rng(2 + rank).standard_normal(2 * nloc)).to(dev)])
+    u, old, prev = (sp.wrap([torch.from_numpy(mk(n)).to(dev) for n in nlocs]) for _ in range(3))
+    v = sp.wrap([torch.from_numpy(np.random.default_rng(2 + rank).standard_normal(2 * n)).to(dev) for n in nlocs])
     res = SlabResidual(grp, old, prev, sc)
     unorm = sp.norm(u)
     stream = torch.cuda.current_stream()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+
+    def max_ms(ms):
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        if dist is not None:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     def step():
         f = res.device_call(u, check=False)
@@ -268,63 +282,65 @@ def run_slabs(args, w, rank, world, local, dist):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
-    dist.barrier()
+    barrier()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(stream)
     for _ in range(args.steps):
         step()
     b.record(stream)
     torch.cuda.synchronize()
-    dist.barrier()
+    barrier()
     clk.__exit__()
-    t = torch.tensor([a.elapsed_time(b) / args.steps], device=dev, dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    ms = max_ms(a.elapsed_time(b) / args.steps)
     D_glob = 2 * int(np.prod([c + 1 for c in counts]))
     value = 2 * D_glob / (ms * 1e-3) / 1e6
 
     # end to end through the slab API with this rank's host buffers: upload
     # u, v from pinned memory, residual + Jv, download F and Jv, every step
-    u_pin = u.parts[0].cpu().pin_memory()
-    v_pin = v.parts[0].cpu().pin_memory()
-    f_pin = torch.empty_like(u_pin).pin_memory()
-    j_pin = torch.empty_like(u_pin).pin_memory()
-    u_d, v_d = torch.empty_like(u.parts[0]), torch.empty_like(v.parts[0])
+    u_pin = [p.cpu().pin_memory() for p in u.parts]
+    v_pin = [p.cpu().pin_memory() for p in v.parts]
+    f_pin = [torch.empty_like(p).pin_memory() for p in u_pin]
+    j_pin = [torch.empty_like(p).pin_memory() for p in u_pin]
+    u_d = [torch.empty_like(p) for p in u.parts]
+    v_d = [torch.empty_like(p) for p in v.parts]
 
     def e2e_step():
-        u_d.copy_(u_pin, non_blocking=True)
-        v_d.copy_(v_pin, non_blocking=True)
-        uu, vv = sp.wrap([u_d]), sp.wrap([v_d])
+        for i in range(len(u_d)):
+            u_d[i].copy_(u_pin[i], non_blocking=True)
+            v_d[i].copy_(v_pin[i], non_blocking=True)
+        uu, vv = sp.wrap(list(u_d)), sp.wrap(list(v_d))
         f = res.device_call(uu, check=False)
         jv = res.jv_device(uu, f, vv, sp.norm(uu))
-        f_pin.copy_(f.parts[0], non_blocking=True)
-        j_pin.copy_(jv.parts[0], non_blocking=True)
+        for i in range(len(u_d)):
+            f_pin[i].copy_(f.parts[i], non_blocking=True)
+            j_pin[i].copy_(jv.parts[i], non_blocking=True)
 
     for _ in range(args.warmup):
         e2e_step()
     torch.cuda.synchronize()
-    dist.barrier()
+    barrier()
     a.record(stream)
     for _ in range(args.steps):
         e2e_step()
     b.record(stream)
     torch.cuda.synchronize()
-    dist.barrier()
-    t = torch.tensor([a.elapsed_time(b) / args.steps], device=dev, dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_ms = float(t.item())
+    barrier()
+    e2e_ms = max_ms(a.elapsed_time(b) / args.steps)
+    nb = 2 * 2 * sum(nlocs) * 8
     e2e = {"value": round(2 * D_glob / (e2e_ms * 1e-3) / 1e6, 2), "unit": "MDoF/s",
-           "h2d_bytes_per_step": 2 * 2 * nloc * 8, "d2h_bytes_per_step": 2 * 2 * nloc * 8,
-           "ms_per_step": round(e2e_ms, 3), "note": "per rank (its slab), max over ranks"}
+           "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb,
+           "ms_per_step": round(e2e_ms, 3), "note": "per rank (its slabs), max over ranks"}
     if rank == 0:
         line = {
             "metric": "MDoF/s residual+Jv fill", "value": round(value, 2), "unit": "MDoF/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+            "n_gpus": 1 if emulate else world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": round(ms, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": args.workload, "model": w["model"], "dim": w["dim"], "counts": counts,
                        "dof": D_glob, "dof_per_step": 2 * D_glob,
-                       "parallelism": f"slab x{world} (NCCL ghost planes + allreduce)",
+                       "parallelism": (f"slab x{nslab} emulated in one process (testing)" if emulate
+                                       else f"slab x{world} (NCCL ghost planes + allreduce)"),
                        "l2": "per-rank inputs larger than L2; no flush"},
             "gpu_launches": 5 * args.steps, "clocks": clk.summary(), "roofline": None,
             "e2e": e2e, "cpu_baseline": None,
@@ -340,6 +356,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="fg2d_2048", choices=sorted(WORKLOADS))
     ap.add_argument("--no-lex", action="store_true", help="skip the lexicographic-ordering Newton solve")
+    ap.add_argument("--emulate-slabs", type=int, default=0,
+                    help="testing: run the N>1 slab path with K slabs in this process on one GPU")
     ap.add_argument("--no-newton", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
@@ -358,6 +376,9 @@ def main():
 
     torch.cuda.set_device(local)
     dist = None
+    if args.emulate_slabs > 1 and world == 1:
+        run_slabs(args, w, rank, world, local, None, emulate=args.emulate_slabs)
+        return
     if world > 1:
         import torch.distributed as dist
 
