@@ -205,7 +205,7 @@ def vcycle_bytes(pc, N, dim):
 
     total = 0.0
 
-    # stencil rows of uniform tiles are not read (one shared row per level)
+    # uniform stencil rows are not read (one shared row per level)
     stencil = [8 * K * (1.0 - 0.5 * (pc.uniform_fraction(l, 0) + pc.uniform_fraction(l, 1)))
                for l in range(len(rows))]
 

@@ -201,8 +201,9 @@ int uc_precond_apply(uc_ctx* ctx, const double* v, double* out);
  * row order, offsets (dx,dy[,dz]) lexicographic with dx fastest. */
 int uc_precond_stencil(uc_ctx* ctx, int level, int block, double* host_out);
 int uc_precond_levels(uc_ctx* ctx, int64_t* shapes /* [levels][3] */);
-/* Fraction of 32-row stencil tiles of (level, block) that are bitwise equal to
- * an interior row, so the apply kernels skip their loads (synchronises). */
+/* Fraction of the owned stencil rows of (level, block) that are bitwise equal
+ * to an interior row, so the apply kernels read that one shared row instead of
+ * their own (synchronises). */
 int uc_precond_uniform(uc_ctx* ctx, int level, int block, double* frac);
 
 /* On-device initial conditions over the context's owned planes (SURVEY 8(f)

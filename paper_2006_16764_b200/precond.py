@@ -136,7 +136,7 @@ class BlockPrecond:
         return out
 
     def uniform_fraction(self, level: int, block: int) -> float:
-        """Share of stencil tiles the apply kernels read from one shared row."""
+        """Share of stencil rows the apply kernels read from one shared row."""
         out = C.c_double()
         L.check(self._ctx.lib.uc_precond_uniform(self._ctx.bind(), level, block, C.byref(out)),
                 "uc_precond_uniform")

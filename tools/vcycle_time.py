@@ -18,13 +18,14 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--counts", type=int, nargs="+", default=[2048, 2048])
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--ordering", default="multicolor")
+ap.add_argument("--builds", type=int, default=3)
 a = ap.parse_args()
 mesh = uc.build_mesh(len(a.counts), [0.03 * c for c in a.counts], a.counts)
 k = uc.FreeGrowthKernel()
 u0 = torch.tensor(seed_initial_condition(mesh, k.params), device="cuda")
 sc = uc.ThetaScheme(1.0, 2.25e-4, 0)
 pc = None
-for rep in range(3):
+for rep in range(a.builds):
     pc = None  # recycle the previous hierarchy (buffers + captured graph)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
