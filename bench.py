@@ -176,7 +176,8 @@ def run_reference(args, w, rank, world):
     mdofs = 2 * D / sec / 1e6
     line = {
         "impl": "reference", "metric": "MDoF/s residual+Jv fill", "value": round(mdofs, 4),
-        "unit": "MDoF/s", "n_gpus": 0, "steps": args.steps, "warmup": args.warmup,
+        "unit": "MDoF/s", "n_gpus": args.gpus, "device": "host cores only", "steps": args.steps,
+        "warmup": args.warmup,
         "ms_per_step": round(sec * 1e3, 3), "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.workload, **{k: w[k] for k in ("model", "dim", "counts")}},
