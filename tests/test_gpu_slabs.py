@@ -3,6 +3,8 @@ process exchange ghost planes with stream copies through the same kernels and
 exchange points as the NCCL transport.  Checked against the unsplit device
 path and the reference goldens."""
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -126,3 +128,27 @@ def test_slab_3d_newton_matches_reference(uc):
         prev, state = state, u
     assert newton == m["newton"] and gm == m["gmres"]
     assert rel(grp.join(state).cpu().numpy(), golden("run_fg3d_16_3")["state"]) <= 1e-8
+
+
+def test_nccl_transport_loads_and_initialises():
+    """The library's NCCL transport (csrc/comm.cu: dlopen of torch's libnccl,
+    unique id, communicator init/finalize) on the GPU box, one rank (a second
+    rank on the same GPU is refused by NCCL).  In a subprocess: the
+    communicator is process-global."""
+    import subprocess
+    import sys
+
+    code = (
+        "import ctypes as C\n"
+        "from paper_2006_16764_b200 import _lib as L\n"
+        "from paper_2006_16764_b200.parallel import nccl_library_path\n"
+        "lib = L.load(); path = nccl_library_path().encode()\n"
+        "idb = (C.c_char * 128)()\n"
+        "L.check(lib.uc_nccl_unique_id(path, idb), 'uc_nccl_unique_id')\n"
+        "L.check(lib.uc_comm_init_nccl(path, idb, 0, 1), 'uc_comm_init_nccl')\n"
+        "assert lib.uc_comm_init_nccl(path, idb, 0, 1) != 0  # second init refused\n"
+        "L.check(lib.uc_comm_finalize(), 'uc_comm_finalize')\n"
+        "print('nccl ok')\n")
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert r.returncode == 0 and "nccl ok" in r.stdout, r.stderr[-2000:]
