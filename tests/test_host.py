@@ -154,3 +154,23 @@ def test_run_config_error_exit_code(tmp_path):
     cfg.output.directory = str(tmp_path / "out")
     code, res = run(cfg)
     assert code == EXIT_CONFIG and res.status == "config_error"
+
+
+def test_no_cpu_fallback_without_a_gpu():
+    """The product path has no CPU implementation: without a CUDA device every
+    compute entry point fails loudly instead of computing on the host."""
+    import torch
+
+    if torch.cuda.is_available():
+        pytest.skip("checks the no-GPU behaviour")
+    import paper_2006_16764_b200 as uc
+    from paper_2006_16764_b200 import _lib as L
+
+    mesh = uc.build_mesh(2, (0.96, 0.96), (8, 8))
+    k = uc.FreeGrowthKernel()
+    st = np.concatenate([np.full(mesh.n_nodes, 0.5), np.ones(mesh.n_nodes)])
+    sc = uc.ThetaScheme(0.5, 2.25e-4, 1)
+    with pytest.raises((L.UcError, RuntimeError)):
+        uc.TimestepResidual(mesh, k, st, st, sc)(st)
+    with pytest.raises((L.UcError, RuntimeError)):
+        uc.build_precond(mesh, k, st, sc)
