@@ -95,6 +95,7 @@ typedef struct uc_scheme {
 #define UC_ORDER_MULTICOLOR 0
 #define UC_ORDER_LEXICOGRAPHIC 1
 #define UC_ORDER_LEXICOGRAPHIC_WAVEFRONT 2  /* same sweep, grid-barrier wavefront kernel (validation) */
+#define UC_ORDER_LEXICOGRAPHIC_ROWS 3       /* same sweep, 3D: every row streams its own stencil (validation) */
 typedef struct uc_precond_cfg {
   int32_t kind;           /* UC_PC_* */
   int32_t sweeps;

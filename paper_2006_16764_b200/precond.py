@@ -183,6 +183,8 @@ def build_precond(mesh, kernel, state, scheme, config: PrecondConfig | None = No
     pc.ordering = 1 if cfg.ordering == "lexicographic" else 0
     if pc.ordering == 1 and os.environ.get("UC_LEX_WAVEFRONT") == "1":
         pc.ordering = 2  # the same sweep on the grid-barrier wavefront kernel (validation)
+    elif pc.ordering == 1 and os.environ.get("UC_LEX3_ROWS") == "1":
+        pc.ordering = 3  # 3D: the same sweep streaming every row's own stencil (validation)
     sc = scheme_struct(scheme)
     rc = ctx.lib.uc_precond_build(ctx.bind(), C.byref(sc), L.ptr(st), C.byref(pc))
     if rc == L.UC_ERR_ARG:

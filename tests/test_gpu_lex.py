@@ -1,4 +1,5 @@
-"""Pipelined lexicographic Gauss-Seidel (csrc/precond.cu k_lex_pipe) against
+"""Pipelined lexicographic Gauss-Seidel (csrc/precond.cu k_lex2d in 2D,
+k_lex_pipe3 with shared class rows and k_lex_pipe in 3D) against
 the grid-barrier wavefront kernel that executes the reference's sequential
 sweep front by front (k_sgs_lex, precond.py:32-51): applications must be
 BITWISE identical -- same subtraction order, correctly rounded division --
@@ -14,7 +15,7 @@ import torch
 pytestmark = pytest.mark.gpu
 
 CASES = [(2, (16, 12)), (2, (64, 40)), (2, (33, 95)), (2, (100, 70)),
-         (3, (8, 6, 5)), (3, (16, 16, 16)), (3, (40, 36, 10))]
+         (3, (8, 6, 5)), (3, (16, 16, 16)), (3, (40, 36, 10)), (3, (24, 70, 20))]
 
 
 def _apply(uc, mesh, k, st, v, wavefront, kind):
@@ -51,6 +52,13 @@ def test_pipelined_lexicographic_is_bitwise_the_sequential_sweep(dim, counts, mo
         a = _apply(uc, mesh, k, st, v, False, kind)
         b = _apply(uc, mesh, k, st, v, True, kind)
         assert torch.equal(a, b), (kind, float((a - b).abs().max()))
+        if dim == 3:
+            os.environ["UC_LEX3_ROWS"] = "1"
+            try:
+                c = _apply(uc, mesh, k, st, v, False, kind)
+            finally:
+                del os.environ["UC_LEX3_ROWS"]
+            assert torch.equal(a, c), (kind, float((a - c).abs().max()))
 
 
 @pytest.mark.parametrize("dim,counts,model", [(2, (64, 40), "free_growth"), (2, (33, 95), "alloy"),
