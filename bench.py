@@ -57,6 +57,9 @@ WORKLOADS = {
                      theta=0.5, dt=2.25e-4, step=2),
     "fg3d_512": dict(model="free_growth", dim=3, extents=(15.36,) * 3, counts=(512,) * 3,
                      theta=0.5, dt=2.25e-4, step=2),
+    # not a BASELINE config: alloy 3D for kernel tuning
+    "al3d_128": dict(model="alloy", dim=3, extents=(102.4,) * 3, counts=(128,) * 3,
+                     theta=0.5, dt=0.002, step=2),
 }
 
 
