@@ -596,7 +596,7 @@ def main():
             sc0 = uc.ThetaScheme(1.0, w["dt"], 0)
             walls = []
             pc = r0 = None
-            for rep_i in range(2):  # cold (first) and warm (allocator/JIT warm) solves
+            for rep_i in range(4):  # cold (first) and three warm solves (median: host jitter)
                 pc = r0 = None  # recycle the previous hierarchy (precond._pool)
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
@@ -609,7 +609,7 @@ def main():
                 _, rep = uc.newton_solve(r0, st, uc.NewtonConfig(), precond_apply=pc.apply)
                 torch.cuda.synchronize()
                 walls.append(time.perf_counter() - t0)
-            t_newton = walls[-1]
+            t_newton = float(np.median(walls[1:]))
             vv = torch.randn_like(st)
             t_apply = timed(lambda: pc.device_apply(vv, check=False), 5)
             vb = vcycle_bytes(pc, N, w["dim"])
