@@ -140,8 +140,10 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.rows), "source": self.source}
 
 
-def cpu_oracle_step_time(w, steps=2, warmup=1, rows=None):
-    """Residual + Jv of the oracle port on the host; returns (sec/step, D, sample)."""
+def cpu_oracle_step_time(w, steps=2, warmup=1, rows=None, min_seconds=0.0):
+    """Residual + Jv of the oracle port on the host; returns (sec/step, D, sample).
+    With min_seconds, keeps timing steps until that much CPU time has been
+    measured (at least `steps`)."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import oracle as O
     from paper_2006_16764_b200 import AlloyParams, FreeGrowthParams
@@ -160,12 +162,16 @@ def cpu_oracle_step_time(w, steps=2, warmup=1, rows=None):
     p = O.Problem(w["dim"], wl["extents"], wl["counts"], w["model"], params, w["theta"], w["dt"], w["step"])
     p.begin(old, prev)
     times = []
-    for i in range(warmup + steps):
+    i = 0
+    while i < warmup + steps or sum(times) < min_seconds:
         t0 = time.perf_counter()
         f = p.residual(u)
         p.jv(u, f, v)
         if i >= warmup:
             times.append(time.perf_counter() - t0)
+        i += 1
+    if min_seconds > 0.0:
+        sample += f", {len(times)} timed steps ({sum(times):.1f} s)"
     return float(np.mean(times)), 2 * N, sample, O.num_threads()
 
 
@@ -659,7 +665,8 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             sec, Dc, sample, cores = cpu_oracle_step_time(w, steps=1, warmup=1,
-                                                         rows=None if w["dim"] == 2 and N <= 2049 ** 2 else 128)
+                                                         rows=None if w["dim"] == 2 and N <= 2049 ** 2 else 128,
+                                                         min_seconds=10.0)
             cpu = {"value": round(2 * Dc / sec / 1e6, 4), "unit": "MDoF/s", "cores": cores,
                    "kind": "port", "sample": sample + "; residual+Jv of oracle/uc_oracle.c (OpenMP)"}
         except Exception as exc:  # reported, not fatal
