@@ -50,3 +50,15 @@ def test_our_arm_json_line():
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     nw = d["newton"]
     assert nw["converged"] and nw["newton_iterations"] >= 1
+
+
+@pytest.mark.gpu
+def test_slab_path_json_line():
+    """The N > 1 path of bench.py (one slab per rank, ghost planes and global
+    reductions through the slab group) driven as 2 slabs in one process."""
+    d = _run("--workload", "fg2d_512", "--steps", "3", "--warmup", "3", "--no-cpu-baseline", "--emulate-slabs", "2")
+    assert BASE_KEYS <= set(d)
+    assert d["value"] > 0 and d["scaling"] == "weak"
+    assert "slab x2" in d["config"]["parallelism"]
+    assert d["config"]["counts"] == [512, 1024]  # weak scaling: the slow axis grows with the slab count
+    assert d["e2e"]["value"] > 0
