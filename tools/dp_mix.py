@@ -1,7 +1,7 @@
 """profiles/dp_inst_per_element.json from the ncu instruction-mix capture of
 tools/kernel_mix.py (see tools/gpu_round1c.sh):
 
-    python tools/dp_mix.py gpurun_out/r1c/mix.csv > profiles/dp_inst_per_element.json
+    python tools/dp_mix.py profiles/r01/kernel_mix_ncu.csv > profiles/dp_inst_per_element.json
 """
 import collections
 import csv
