@@ -36,6 +36,7 @@ extern "C" {
 
 #define UC_MODEL_FREE_GROWTH 1
 #define UC_MODEL_ALLOY 2
+#define UC_MODEL_MASS_DIFF 3  /* single-field mass + diffusion test model (tests/test_assembly.py:22-49) */
 
 #define UC_PART_NEW 0
 #define UC_PART_OLD 1
@@ -82,6 +83,8 @@ typedef struct uc_model_params {
   double dcoef;           /* diffusivity */
   double g4_coef;         /* frame_coefficient */
   double pull_velocity;
+  /* mass-diffusion (dcoef = diffusivity) */
+  double mass_coef;       /* 1: (du/dt, psi) term present, 0: diffusion only */
 } uc_model_params;
 
 /* ThetaScheme (undercool/stepping.py:12-37). */

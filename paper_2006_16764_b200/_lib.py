@@ -14,7 +14,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "libuc_b200.so")
 
 UC_OK, UC_ERR_NONFINITE, UC_ERR_ARG, UC_ERR_CUDA, UC_ERR_UNSUPPORTED = 0, 1, 2, 3, 4
-UC_MODEL_FREE_GROWTH, UC_MODEL_ALLOY = 1, 2
+UC_MODEL_FREE_GROWTH, UC_MODEL_ALLOY, UC_MODEL_MASS_DIFF = 1, 2, 3
 UC_PART_NEW, UC_PART_OLD = 0, 1
 UC_PC_IDENTITY, UC_PC_JACOBI, UC_PC_SGS, UC_PC_VCYCLE = 0, 1, 2, 3
 
@@ -30,7 +30,8 @@ class ModelParams(C.Structure):
                 ("beta", C.c_double), ("alpha", C.c_double), ("latent", C.c_double),
                 ("hcell", C.c_double), ("tmelt", C.c_double), ("at_reg2", C.c_double),
                 ("kpart", C.c_double), ("coupling", C.c_double), ("dcoef", C.c_double),
-                ("g4_coef", C.c_double), ("pull_velocity", C.c_double)]
+                ("g4_coef", C.c_double), ("pull_velocity", C.c_double),
+                ("mass_coef", C.c_double)]
 
 
 class Scheme(C.Structure):

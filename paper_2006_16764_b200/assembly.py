@@ -21,6 +21,7 @@ import torch
 from . import _lib as L
 from .device import as_device, context_for, is_device, to_host
 from .errors import NonFiniteResidualError
+from .models import n_fields_of
 
 __all__ = ["StateHistory", "split_fields", "join_fields", "assemble_residual",
            "TimestepResidual", "NonFiniteResidualError", "scheme_struct"]
@@ -87,7 +88,7 @@ class TimestepResidual:
         self.old = as_device(old)
         self.prev = as_device(prev)
         self._sc = scheme_struct(scheme)
-        n2 = 2 * self.ctx.n_local
+        n2 = n_fields_of(kernel) * self.ctx.n_local
         if self.old.numel() != n2 or self.prev.numel() != n2:
             raise ValueError(f"state vectors must hold {n2} values")
         fixed = torch.empty_like(self.old)

@@ -68,8 +68,12 @@ const char* uc_last_error(void) { return g_err; }
 int uc_ctx_create(const uc_mesh_desc* mesh, const uc_model_params* params, void* stream,
                   uc_ctx** out) {
   if (!mesh || !params || !out) return set_error(UC_ERR_ARG, "uc_ctx_create: NULL argument");
-  if (params->model != UC_MODEL_FREE_GROWTH && params->model != UC_MODEL_ALLOY)
+  if (params->model != UC_MODEL_FREE_GROWTH && params->model != UC_MODEL_ALLOY &&
+      params->model != UC_MODEL_MASS_DIFF)
     return set_error(UC_ERR_UNSUPPORTED, "unknown model %d", params->model);
+  if (params->model == UC_MODEL_MASS_DIFF &&
+      (mesh->slab_lo != 0 || mesh->slab_hi != mesh->counts[mesh->dim > 0 ? mesh->dim - 1 : 0] + 1))
+    return set_error(UC_ERR_UNSUPPORTED, "the mass-diffusion test model runs on a single slab only");
   uc_ctx* c = new uc_ctx();
   int rc = build_grid(mesh, &c->grid);
   if (rc) {
@@ -206,7 +210,7 @@ int uc_jv_group(uc_ctx* const* ctxs, int n, const uc_scheme* sc, const double* c
   const bool sum = group_needs_sum(G);
   for (int i = 0; i < n; ++i) {
     vn[i] = G[i]->scal + (UC_SCAL_SLOTS - 1);
-    if ((rc = reduce_dot(G[i], 2 * G[i]->grid.nloc, v[i], nullptr, vn[i], !sum))) return rc;
+    if ((rc = reduce_dot(G[i], vec_len(G[i]), v[i], nullptr, vn[i], !sum))) return rc;
   }
   if (sum && (rc = global_sum(G, vn.data(), true, s))) return rc;
   const double eps_num = UC_EPS0 * sqrt(1.0 + unorm);
@@ -232,7 +236,7 @@ int uc_dot_group(uc_ctx* const* ctxs, int n, const double* const* a, const doubl
   int rc;
   for (int i = 0; i < n; ++i) {
     slot[i] = G[i]->scal + (UC_SCAL_SLOTS - 2);
-    if ((rc = reduce_dot(G[i], 2 * G[i]->grid.nloc, a[i], b ? b[i] : nullptr, slot[i], false))) return rc;
+    if ((rc = reduce_dot(G[i], vec_len(G[i]), a[i], b ? b[i] : nullptr, slot[i], false))) return rc;
   }
   if ((rc = global_sum(G, slot.data(), do_sqrt != 0, s))) return rc;
   UC_CUDA_OK(cudaMemcpyAsync(G[0]->pinned, slot[0], sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -244,6 +248,8 @@ int uc_dot_group(uc_ctx* const* ctxs, int n, const double* const* a, const doubl
 int uc_precond_build_group(uc_ctx* const* ctxs, int n, const uc_scheme* sc,
                            const double* const* states, const uc_precond_cfg* cfg) {
   if (!ctxs || n < 1 || !sc || !states || !cfg) return set_error(UC_ERR_ARG, "uc_precond_build: NULL argument");
+  if (ctxs[0]->params.model == UC_MODEL_MASS_DIFF)
+    return set_error(UC_ERR_UNSUPPORTED, "the mass-diffusion test model has no preconditioner coefficients");
   Group G(ctxs, ctxs + n);
   return precond_build_group(G, sc, states, cfg);
 }

@@ -293,7 +293,7 @@ int uc_arnoldi_group(uc_ctx* const* ctxs, int nslabs, const double* const* basis
   std::vector<int64_t> n(nslabs);
   std::vector<const double* const*> b(nslabs);
   for (int i = 0; i < nslabs; ++i) {
-    n[i] = 2 * G[i]->grid.nloc;
+    n[i] = vec_len(G[i]);
     b[i] = basis + (size_t)i * (k + 2);
   }
   return arnoldi_group(G, n.data(), b.data(), k, w, scale, h_host, broke);

@@ -99,6 +99,17 @@ int launch_residual(uc_ctx* c, const uc_scheme* sc, int mode, const double* u,
                     double* eps_out);
 int locate_nonfinite(uc_ctx* c, const uc_scheme* sc, int part, const double* u,
                      const double* old, const double* prev, int64_t out[5]);
+void make_jxw(const Grid& g, double* jxw);
+// massdiff.cu (single-field test model)
+int launch_massdiff(uc_ctx* c, const uc_scheme* sc, int mode, const double* u, const double* old,
+                    const double* v, const double* fu, const double* fixed, double* out,
+                    double eps_num, const double* vnorm_dev, double* eps_out);
+int locate_massdiff(uc_ctx* c, const uc_scheme* sc, int mode, const double* u, const double* old,
+                    unsigned long long* key_dev);
+// entries per vector: fields x owned nodes
+inline int64_t vec_len(const uc_ctx* c) {
+  return (c->params.model == UC_MODEL_MASS_DIFF ? 1 : 2) * c->grid.nloc;
+}
 // precond.cu
 int precond_build(uc_ctx* c, const uc_scheme* sc, const double* state, const uc_precond_cfg* cfg);
 int precond_build_group(const Group& G, const uc_scheme* sc, const double* const* states,

@@ -17,7 +17,7 @@ from dataclasses import dataclass
 from . import _lib as L
 
 __all__ = ["FreeGrowthParams", "FreeGrowthKernel", "AlloyParams", "AlloyKernel",
-           "device_params", "model_of"]
+           "MassDiffKernel", "device_params", "model_of", "n_fields_of"]
 
 # thin-interface constants of the dilute-alloy model (alloy.py:31-33)
 A1 = 0.8839
@@ -156,6 +156,44 @@ class AlloyKernel:
                 "solute_diffusivity": p.diffusivity, "solute_d0": p.solute_d0}
 
 
+def is_mass_diff(kernel) -> bool:
+    """The reference's single-field assembly test plug-in (tests/test_assembly.py:22-49)
+    or this package's MassDiffKernel, recognised by name and attributes.  A
+    subclass that overrides residual_gauss runs its own Python physics and is
+    not recognised (no CPU fallback)."""
+    name = type(kernel).__name__
+    if name != "MassDiffKernel" and not isinstance(kernel, MassDiffKernel):
+        return False
+    if not (hasattr(kernel, "c") and hasattr(kernel, "mass") and getattr(kernel, "n_fields", 0) == 1):
+        return False
+    # a subclass with its own residual_gauss is a different model
+    for klass in type(kernel).__mro__:
+        if "residual_gauss" in vars(klass):
+            return klass.__name__ == "MassDiffKernel"
+    return True
+
+
+class MassDiffKernel:
+    """Single-field theta-method model (du/dt, psi) + (c grad u, grad psi): the
+    reference's assembly test plug-in (tests/test_assembly.py:22-49), assembled
+    on the device by csrc/massdiff.cu.  No preconditioner coefficients (the
+    reference's plug-in has none either)."""
+
+    n_fields = 1
+    field_names = ("u",)
+    contour_level = 0.5
+    needs_rate = False
+    needs_old_value = False
+
+    def __init__(self, diffusivity=1.0, mass=True):
+        self.c = diffusivity
+        self.mass = mass
+
+
+def n_fields_of(kernel) -> int:
+    return 1 if model_of(kernel) == L.UC_MODEL_MASS_DIFF else 2
+
+
 def model_of(kernel) -> int:
     """UC_MODEL_* for a kernel object of this package or the reference."""
     name = type(kernel).__name__
@@ -164,6 +202,8 @@ def model_of(kernel) -> int:
         return L.UC_MODEL_FREE_GROWTH
     if name == "AlloyKernel" and p is not None and hasattr(p, "partition"):
         return L.UC_MODEL_ALLOY
+    if is_mass_diff(kernel):
+        return L.UC_MODEL_MASS_DIFF
     raise NotImplementedError(
         f"kernel {name!r} has no device implementation; only the built-in free-growth "
         "and alloy models run on the B200 path (no CPU fallback)")
@@ -174,9 +214,13 @@ def device_params(kernel) -> L.ModelParams:
     expressions as the reference's wrappers (free_growth.py:176-200,
     alloy.py:239-265)."""
     model = model_of(kernel)
-    p = kernel.params
     mp = L.ModelParams()
     mp.model = model
+    if model == L.UC_MODEL_MASS_DIFF:
+        mp.dcoef = float(kernel.c)
+        mp.mass_coef = 1.0 if kernel.mass else 0.0
+        return mp
+    p = kernel.params
     mp.eps = p.anisotropy_strength
     mp.reg = p.aniso_reg_grad ** 4
     mp.aniso_reg_grad = p.aniso_reg_grad

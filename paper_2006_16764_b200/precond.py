@@ -29,6 +29,7 @@ import torch
 from . import _lib as L
 from . import device as D
 from .assembly import scheme_struct
+from .models import model_of
 
 __all__ = ["PrecondConfig", "BlockPrecond", "build_precond", "apply_precond"]
 
@@ -175,6 +176,8 @@ def build_precond(mesh, kernel, state, scheme, config: PrecondConfig | None = No
     cfg = config or PrecondConfig()
     if cfg.kind == "direct":
         raise NotImplementedError("kind='direct' (SuperLU) has no device implementation")
+    if model_of(kernel) == L.UC_MODEL_MASS_DIFF:
+        raise NotImplementedError("the mass-diffusion test model has no preconditioner coefficients")
     ctx, key = _pool_take(mesh, kernel)
     st = D.as_device(state)
     pc = L.PrecondCfg()

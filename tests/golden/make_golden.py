@@ -17,6 +17,7 @@ Reference entry points exercised (file:line under /root/reference/pkg/src/underc
   gmres_solve                  krylov.py:81-208
   newton_solve                 newton.py:116-198
   simulate (iteration counts)  driver.py:135-242
+  MassDiffKernel test plug-in  tests/test_assembly.py:22-49 (massdiff_cases)
   simulate records / outcomes  driver.py:186-229 (driver_cases)
   _heat_balance, _total_solute driver.py:76-98, extract_tip diagnostics.py:69-89
 """
@@ -413,8 +414,60 @@ def writer_cases(meta):
     meta["writers"] = info
 
 
+MASSDIFF_CASES = [
+    # name, dim, extents, counts, diffusivity, mass, theta, dt
+    ("md2d", 2, (1.2, 0.8), (12, 10), 0.7, True, 0.5, 0.05),
+    ("md2d_nomass", 2, (2.0, 1.0), (8, 6), 1.3, False, 1.0, 0.1),
+    ("md3d", 3, (0.6, 0.5, 0.4), (5, 4, 3), 0.9, True, 0.6, 0.02),
+]
+
+
+def massdiff_cases(meta):
+    """The reference's single-field assembly test plug-in (tests/test_assembly.py:22-49)
+    run through assemble_residual (all three parts), TimestepResidual, jfnk_matvec
+    and an unpreconditioned newton_solve."""
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location(
+        "ref_test_assembly", os.path.join(os.path.dirname(REF), "tests", "test_assembly.py"))
+    mod = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mod)
+    MassDiffKernel = mod.MassDiffKernel
+    from undercool.assembly import TimestepResidual
+    from undercool.newton import jfnk_matvec, newton_solve
+    from undercool.stepping import ThetaScheme
+
+    for name, dim, ext, cnt, c, mass, theta, dt in MASSDIFF_CASES:
+        mesh = uc.build_mesh(dim, list(ext), list(cnt))
+        k = MassDiffKernel(diffusivity=c, mass=mass)
+        rng = np.random.default_rng(21)
+        n = mesh.n_nodes
+        new, old, prev, v = (rng.standard_normal(n) for _ in range(4))
+        sc = ThetaScheme(theta, dt, 0)
+        st = StateHistory(new, old, prev)
+        out = {p: assemble_residual(mesh, k, st, sc, part=p) for p in ("old", "new", "full")}
+        res = TimestepResidual(mesh, k, old, prev, sc)
+        fu = res(new)
+        jv = jfnk_matvec(res, new, fu, v)
+        res2 = TimestepResidual(mesh, k, old, prev, sc)
+        u, rep = newton_solve(res2, old.copy())
+        np.savez(os.path.join(OUT, f"massdiff_{name}.npz"), new=new, old=old, prev=prev, v=v,
+                 r_old=out["old"], r_new=out["new"], r_full=out["full"], fixed=res.fixed_part,
+                 fu=fu, jv=jv, newton_u=u)
+        meta[f"massdiff_{name}"] = dict(dim=dim, extents=ext, counts=cnt, diffusivity=c, mass=mass,
+                                        theta=theta, dt=dt, newton=rep.iterations,
+                                        gmres=rep.gmres_iterations, converged=rep.converged)
+        print(name, rep.iterations, rep.gmres_iterations, rep.converged)
+
+
 def main():
     meta = {"generator": "tests/golden/make_golden.py", "reference": REF}
+    if "--only-massdiff" in sys.argv:
+        meta = json.load(open(os.path.join(OUT, "golden.json")))
+        massdiff_cases(meta)
+        with open(os.path.join(OUT, "golden.json"), "w") as fh:
+            json.dump(meta, fh, indent=1, sort_keys=True)
+        return
     if "--only-writers" in sys.argv:
         meta = json.load(open(os.path.join(OUT, "golden.json")))
         writer_cases(meta)
@@ -431,6 +484,7 @@ def main():
         return
     if "--only-runs" not in sys.argv:
         residual_cases(meta)
+        massdiff_cases(meta)
         precond_cases(meta)
         newton_case(meta)
         ic_cases(meta)
