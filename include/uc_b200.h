@@ -147,6 +147,21 @@ int uc_residual(uc_ctx* ctx, const uc_scheme* sc, int part, const double* unew,
  * (assembly.py:174-190).  Synchronises.  Writes field, part (0 value,
  * 1+d flux[d]), element id, quadrature point and first node; returns 0 if
  * every integrand is finite (fields set to -1). */
+/* assemble_residual(..., elements=subset) (assembly.py:214-230 with `elements`):
+ * the same parts, summed over the elements whose byte in element_mask
+ * (n_elements, element-id order) is non-zero.  part = UC_PART_OLD: out = old
+ * level; UC_PART_NEW: out = new level + fixed (fixed may be NULL for the new
+ * level alone).  Single slab only; not a hot path (node-centric gather, each
+ * element re-evaluated by its corner nodes). */
+int uc_residual_subset(uc_ctx* ctx, const uc_scheme* sc, int part, const double* unew,
+                       const double* old, const double* prev, const double* fixed,
+                       const uint8_t* element_mask, double* out);
+
+/* uc_locate_nonfinite restricted to the elements of element_mask. */
+int uc_locate_nonfinite_subset(uc_ctx* ctx, const uc_scheme* sc, int part, const double* unew,
+                               const double* old, const double* prev, const uint8_t* element_mask,
+                               int64_t* field, int64_t* which, int64_t* element, int64_t* qp,
+                               int64_t* first_node);
 int uc_locate_nonfinite(uc_ctx* ctx, const uc_scheme* sc, int part,
                         const double* unew, const double* old, const double* prev,
                         int64_t* field, int64_t* which, int64_t* element,

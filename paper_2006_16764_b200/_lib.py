@@ -72,6 +72,8 @@ SIGNATURES = {
     "uc_ghost_ptr": (_P, [_P, _I, _I]),
     "uc_residual": (_I, [_P, C.POINTER(Scheme), _I, _P, _P, _P, _P, _P]),
     "uc_locate_nonfinite": (_I, [_P, C.POINTER(Scheme), _I, _P, _P, _P] + [C.POINTER(_I64)] * 5),
+    "uc_residual_subset": (_I, [_P, C.POINTER(Scheme), _I, _P, _P, _P, _P, _P, _P]),
+    "uc_locate_nonfinite_subset": (_I, [_P, C.POINTER(Scheme), _I, _P, _P, _P, _P] + [C.POINTER(_I64)] * 5),
     "uc_jv": (_I, [_P, C.POINTER(Scheme), _P, _P, _P, _D, _P, _P, _P, _P, _P]),
     "uc_dot": (_I, [_P, _I64, _P, _P, _P]),
     "uc_norm": (_I, [_P, _I64, _P, _P]),

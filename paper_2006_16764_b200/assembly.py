@@ -144,9 +144,12 @@ def assemble_residual(mesh, kernel, states, scheme, rule=None, elements=None, pa
     """Global residual of one theta step (assembly.py:214-230) on the device.
 
     part="old" is the fixed part, part="new" the live part, part="full" their
-    sum.  Element subsets are not supported on the device."""
+    sum.  `elements` (element ids, as the reference's mesh.conn[elements])
+    restricts the sum to those elements (uc_residual_subset); a non-finite
+    report then names the element by its position in `elements`, as the
+    reference's _check_finite does (assembly.py:174-190)."""
     if elements is not None:
-        raise NotImplementedError("element subsets are not assembled on the device")
+        return _assemble_subset(mesh, kernel, states, scheme, rule, elements, part)
     _default_rule(rule)
     ctx = context_for(mesh, kernel)
     host = not is_device(states.old)
@@ -174,3 +177,81 @@ def assemble_residual(mesh, kernel, states, scheme, rule=None, elements=None, pa
         if ctx.status().residual_nonfinite:
             _raise_nonfinite(ctx, sc, L.UC_PART_NEW, new, old, prev)
     return to_host(out) if host else out
+
+
+def _assemble_subset(mesh, kernel, states, scheme, rule, elements, part):
+    _default_rule(rule)
+    if part not in ("old", "new", "full"):
+        raise ValueError(f"unknown part {part!r}")
+    ctx = context_for(mesh, kernel)
+    ids = np.asarray(elements)
+    n_el = int(np.prod(mesh.counts))
+    if ids.dtype == bool:
+        ids = np.nonzero(ids)[0]
+    ids = ids.astype(np.int64).reshape(-1)
+    if ids.size and (ids.min() < 0 or ids.max() >= n_el):
+        raise IndexError("element id out of range")
+    if np.unique(ids).size != ids.size:
+        raise NotImplementedError("repeated element ids are not assembled on the device")
+    mask_h = np.zeros(n_el, dtype=np.uint8)
+    mask_h[ids] = 1
+    mask = torch.from_numpy(mask_h).to("cuda")
+    host = not is_device(states.old)
+    old, prev = as_device(states.old), as_device(states.prev)
+    sc = scheme_struct(scheme)
+    lib = ctx.lib
+
+    def run(pt, u, fixed, out):
+        L.check(lib.uc_residual_subset(ctx.bind(), C.byref(sc), pt, L.ptr(u) if u is not None else None,
+                                       L.ptr(old), L.ptr(prev), L.ptr(fixed) if fixed is not None else None,
+                                       L.ptr(mask), L.ptr(out)), "uc_residual_subset")
+        if ctx.status().residual_nonfinite:
+            _raise_nonfinite_subset(ctx, sc, pt, u, old, prev, mask, ids, mesh)
+
+    fixed = None
+    if part in ("old", "full"):
+        fixed = torch.empty_like(old)
+        run(L.UC_PART_OLD, None, None, fixed)
+        if part == "old":
+            return to_host(fixed) if host else fixed
+    new = as_device(states.new)
+    out = torch.empty_like(old)
+    run(L.UC_PART_NEW, new, fixed, out)
+    return to_host(out) if host else out
+
+
+def _raise_nonfinite_subset(ctx, sc, part, u, old, prev, mask, ids, mesh):
+    """The reference scans field, then integrand part, then (position in the
+    subset, qp) (assembly.py:174-190).  The device locator orders elements by
+    id, so the first position holding the offending (field, part) pair is found
+    by bisection over prefixes of the subset (an error path: O(log n) calls)."""
+
+    def locate(m):
+        r = [C.c_int64() for _ in range(5)]
+        L.check(ctx.lib.uc_locate_nonfinite_subset(
+            ctx.bind(), C.byref(sc), part, L.ptr(u) if u is not None else None, L.ptr(old),
+            L.ptr(prev), L.ptr(m), *[C.byref(x) for x in r]), "uc_locate_nonfinite_subset")
+        return [x.value for x in r]
+
+    def prefix_mask(n):
+        m = torch.zeros_like(mask)
+        m[torch.from_numpy(ids[:n]).to(mask.device)] = 1
+        return m
+
+    f, w, e, q, first = locate(mask)
+    if f < 0:
+        raise NonFiniteResidualError("non-finite residual entry after assembly")
+    lo, hi = 1, len(ids)
+    while lo < hi:  # smallest prefix holding a non-finite (f, w) integrand
+        mid = (lo + hi) // 2
+        r = locate(prefix_mask(mid))
+        if r[0] == f and r[1] == w:
+            hi = mid
+        else:
+            lo = mid + 1
+    f, w, e, q, first = locate(prefix_mask(lo) - prefix_mask(lo - 1))
+    pos = lo - 1
+    name = "value" if w == 0 else f"flux[{w - 1}]"
+    raise NonFiniteResidualError(
+        f"non-finite {name} integrand for field {f} at element {pos} "
+        f"(first node {first}), quadrature point {q}")

@@ -177,6 +177,36 @@ int uc_residual(uc_ctx* c, const uc_scheme* sc, int part, const double* unew, co
   return uc_residual_group(&c, 1, sc, part, &unew, &old, &prev, &fixed, &out);
 }
 
+int uc_residual_subset(uc_ctx* c, const uc_scheme* sc, int part, const double* unew,
+                       const double* old, const double* prev, const double* fixed,
+                       const uint8_t* element_mask, double* out) {
+  if (!c || !sc || !old || !prev || !element_mask || !out)
+    return set_error(UC_ERR_ARG, "uc_residual_subset: NULL argument");
+  if (!(sc->dt > 0.0)) return set_error(UC_ERR_ARG, "uc_residual_subset: bad scheme");
+  if (part != UC_PART_OLD && (part != UC_PART_NEW || !unew))
+    return set_error(UC_ERR_ARG, "uc_residual_subset: bad part");
+  if (c->grid.lo != 0 || c->grid.hi != c->grid.nslow)
+    return set_error(UC_ERR_UNSUPPORTED, "element subsets are assembled on a single slab only");
+  return launch_subset(c, sc, part == UC_PART_OLD ? MODE_OLD : MODE_NEW, unew, old, prev, fixed,
+                       element_mask, out);
+}
+
+int uc_locate_nonfinite_subset(uc_ctx* c, const uc_scheme* sc, int part, const double* unew,
+                               const double* old, const double* prev, const uint8_t* element_mask,
+                               int64_t* field, int64_t* which, int64_t* element, int64_t* qp,
+                               int64_t* first_node) {
+  if (!c || !sc) return set_error(UC_ERR_ARG, "uc_locate_nonfinite: NULL argument");
+  int64_t o[5];
+  int rc = locate_nonfinite(c, sc, part, unew, old, prev, o, element_mask);
+  if (rc < 0 || rc > 1) return rc;
+  *field = o[0];
+  *which = o[1];
+  *element = o[2];
+  *qp = o[3];
+  *first_node = o[4];
+  return UC_OK;
+}
+
 int uc_locate_nonfinite(uc_ctx* c, const uc_scheme* sc, int part, const double* unew,
                         const double* old, const double* prev, int64_t* field, int64_t* which,
                         int64_t* element, int64_t* qp, int64_t* first_node) {

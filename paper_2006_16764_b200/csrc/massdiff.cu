@@ -30,6 +30,7 @@ struct MdArgs {
   double eps_num;
   const double* vnorm;
   double* eps_out;
+  const uint8_t* emask;  // element subset (assemble_residual(elements=...)); NULL = all
 };
 
 // value / gradient weight of local node j = jx + 2jy (+4jz) at qp (qx, qy, qz)
@@ -108,6 +109,7 @@ __global__ void k_massdiff(const __grid_constant__ MdArgs a) {
       for (int bx = 0; bx < 2; ++bx) {
         const int64_t ex = ix - 1 + bx;
         if (ex < 0 || ex >= g.ne[0]) continue;
+        if (a.emask && !a.emask[ex + ey * g.ne[0] + (DIM == 3 ? ez * g.ne[0] * g.ne[1] : 0)]) continue;
         double s[8];
         element_nodes<DIM>(a, ex, ey, DIM == 3 ? ez : 0, eps, s);
         const int me = (1 - bx) + 2 * (1 - by) + (DIM == 3 ? 4 * (1 - bz) : 0);
@@ -131,7 +133,7 @@ __global__ void k_massdiff(const __grid_constant__ MdArgs a) {
   if (MODE == MODE_OLD)
     a.out[i] = live;
   else if (MODE == MODE_NEW)
-    a.out[i] = live + a.fixed[i];
+    a.out[i] = a.fixed ? live + a.fixed[i] : live;
   else
     a.out[i] = __dsub_rn(live + a.fixed[i], a.fu[i]) / eps;
 }
@@ -142,7 +144,7 @@ __global__ void k_massdiff_locate(const __grid_constant__ MdArgs a, unsigned lon
   const Grid& g = a.g;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t ne = g.ne[0] * g.ne[1] * (DIM == 3 ? g.ne[2] : 1);
-  if (e >= ne) return;
+  if (e >= ne || (a.emask && !a.emask[e])) return;
   const int64_t ex = e % g.ne[0];
   const int64_t ey = DIM == 3 ? (e / g.ne[0]) % g.ne[1] : e / g.ne[0];
   const int64_t ez = DIM == 3 ? e / (g.ne[0] * g.ne[1]) : 0;
@@ -206,9 +208,29 @@ int launch_massdiff(uc_ctx* c, const uc_scheme* sc, int mode, const double* u, c
   return UC_OK;
 }
 
-int locate_massdiff(uc_ctx* c, const uc_scheme* sc, int mode, const double* u, const double* old,
-                    unsigned long long* key_dev) {
+int launch_massdiff_subset(uc_ctx* c, const uc_scheme* sc, int mode, const double* u,
+                           const double* old, const double* fixed, const uint8_t* emask, double* out) {
   MdArgs a = make_md(c, sc, mode);
+  a.u = mode == MODE_OLD ? old : u;
+  a.fixed = fixed;
+  a.out = out;
+  a.emask = emask;
+  const unsigned blocks = (unsigned)((c->grid.nloc + 255) / 256);
+  const bool d2 = c->grid.dim == 2;
+  if (mode == MODE_OLD)
+    d2 ? k_massdiff<2, MODE_OLD><<<blocks, 256, 0, c->stream>>>(a)
+       : k_massdiff<3, MODE_OLD><<<blocks, 256, 0, c->stream>>>(a);
+  else
+    d2 ? k_massdiff<2, MODE_NEW><<<blocks, 256, 0, c->stream>>>(a)
+       : k_massdiff<3, MODE_NEW><<<blocks, 256, 0, c->stream>>>(a);
+  UC_CUDA_OK(cudaGetLastError());
+  return UC_OK;
+}
+
+int locate_massdiff(uc_ctx* c, const uc_scheme* sc, int mode, const double* u, const double* old,
+                    const uint8_t* emask, unsigned long long* key_dev) {
+  MdArgs a = make_md(c, sc, mode);
+  a.emask = emask;
   a.u = mode == MODE_OLD ? old : u;
   const Grid& g = c->grid;
   const int64_t ne = g.ne[0] * g.ne[1] * (g.dim == 3 ? g.ne[2] : 1);

@@ -98,14 +98,19 @@ int launch_residual(uc_ctx* c, const uc_scheme* sc, int mode, const double* u,
                     const double* fixed, double* out, double eps_num, const double* vnorm_dev,
                     double* eps_out);
 int locate_nonfinite(uc_ctx* c, const uc_scheme* sc, int part, const double* u,
-                     const double* old, const double* prev, int64_t out[5]);
+                     const double* old, const double* prev, int64_t out[5],
+                     const uint8_t* emask = nullptr);
+int launch_subset(uc_ctx* c, const uc_scheme* sc, int mode, const double* u, const double* old,
+                  const double* prev, const double* fixed, const uint8_t* emask, double* out);
 void make_jxw(const Grid& g, double* jxw);
 // massdiff.cu (single-field test model)
 int launch_massdiff(uc_ctx* c, const uc_scheme* sc, int mode, const double* u, const double* old,
                     const double* v, const double* fu, const double* fixed, double* out,
                     double eps_num, const double* vnorm_dev, double* eps_out);
+int launch_massdiff_subset(uc_ctx* c, const uc_scheme* sc, int mode, const double* u,
+                           const double* old, const double* fixed, const uint8_t* emask, double* out);
 int locate_massdiff(uc_ctx* c, const uc_scheme* sc, int mode, const double* u, const double* old,
-                    unsigned long long* key_dev);
+                    const uint8_t* emask, unsigned long long* key_dev);
 // entries per vector: fields x owned nodes
 inline int64_t vec_len(const uc_ctx* c) {
   return (c->params.model == UC_MODEL_MASS_DIFF ? 1 : 2) * c->grid.nloc;

@@ -460,11 +460,37 @@ def massdiff_cases(meta):
         print(name, rep.iterations, rep.gmres_iterations, rep.converged)
 
 
+def subset_cases(meta):
+    """assemble_residual(..., elements=subset) (assembly.py:214-230) for both
+    models in 2D and 3D: one element colour class and a random subset."""
+    cases = [("fg2d", "free_growth", 2, (0.48, 0.36), (16, 12), 0.5, 3e-4, 2),
+             ("al3d", "alloy", 3, (6.4, 4.8, 3.2), (8, 6, 4), 0.5, 2e-3, 3)]
+    for name, model, dim, ext, cnt, th, dt, step in cases:
+        mesh = uc.build_mesh(dim, list(ext), list(cnt))
+        k = kernel_for(model)
+        rng = np.random.default_rng(31)
+        mk = fg_state if model == "free_growth" else alloy_state
+        new, old, prev = (mk(rng, mesh.n_nodes) for _ in range(3))
+        sc = uc.ThetaScheme(th, dt, step)
+        st = StateHistory(new, old, prev)
+        color = mesh.colors[1]
+        rand = rng.permutation(mesh.n_elements)[: mesh.n_elements // 3]
+        out = dict(new=new, old=old, prev=prev, color=color, rand=rand)
+        for sub in ("color", "rand"):
+            for p in ("old", "new", "full"):
+                out[f"{sub}_{p}"] = assemble_residual(mesh, k, st, sc, elements=out[sub], part=p)
+        np.savez(os.path.join(OUT, f"subset_{name}.npz"), **out)
+        meta[f"subset_{name}"] = dict(model=model, dim=dim, extents=ext, counts=cnt, theta=th, dt=dt,
+                                      step=step)
+        print("subset", name)
+
+
 def main():
     meta = {"generator": "tests/golden/make_golden.py", "reference": REF}
     if "--only-massdiff" in sys.argv:
         meta = json.load(open(os.path.join(OUT, "golden.json")))
         massdiff_cases(meta)
+        subset_cases(meta)
         with open(os.path.join(OUT, "golden.json"), "w") as fh:
             json.dump(meta, fh, indent=1, sort_keys=True)
         return
@@ -485,6 +511,7 @@ def main():
     if "--only-runs" not in sys.argv:
         residual_cases(meta)
         massdiff_cases(meta)
+        subset_cases(meta)
         precond_cases(meta)
         newton_case(meta)
         ic_cases(meta)
