@@ -240,21 +240,25 @@ def vcycle_bytes(pc, N, dim):
 
 
 def run_slabs(args, w, rank, world, local, dist, emulate=0):
-    """N > 1: one slab per GPU of a weak-scaled mesh (counts[-1] x world), NCCL
-    ghost planes and allreduce inside the library (paper_2006_16764_b200.parallel).
-    emulate=K (testing, --emulate-slabs): the same code path with K slabs driven
-    by this one process on one GPU (planes copied on the stream instead of NCCL)."""
+    """N > 1: one slab per GPU (paper_2006_16764_b200.parallel), NCCL ghost
+    planes and allreduces inside the library.  --scaling weak (default): the
+    mesh grows with N (counts[-1] x N, same h: fixed work per GPU); strong: the
+    named mesh is split N ways.  emulate=K (testing, --emulate-slabs): the same
+    code path with K slabs driven by this one process on one GPU (planes copied
+    on the stream instead of NCCL)."""
     import torch
 
     import paper_2006_16764_b200 as uc
-    from paper_2006_16764_b200.parallel import SlabGroup, SlabResidual
+    from paper_2006_16764_b200.models import seed_initial_condition_device
+    from paper_2006_16764_b200.parallel import SlabGroup, SlabPrecond, SlabResidual
 
     dev = torch.device("cuda", local)
     nslab = emulate if emulate else world
     counts = list(w["counts"])
     extents = list(w["extents"])
-    counts[-1] *= nslab
-    extents[-1] *= nslab
+    if args.scaling == "weak":
+        counts[-1] *= nslab
+        extents[-1] *= nslab
     mesh = uc.build_mesh(w["dim"], extents, counts)
     kern = uc.FreeGrowthKernel() if w["model"] == "free_growth" else uc.AlloyKernel()
     sc = uc.ThetaScheme(w["theta"], w["dt"], w["step"])
@@ -275,6 +279,7 @@ def run_slabs(args, w, rank, world, local, dist, emulate=0):
     stream = torch.cuda.current_stream()
 
     def barrier():
+        torch.cuda.synchronize()
         if dist is not None:
             dist.barrier()
 
@@ -288,22 +293,43 @@ def run_slabs(args, w, rank, world, local, dist, emulate=0):
         f = res.device_call(u, check=False)
         return res.jv_device(u, f, v, unorm)
 
+    def timed(fn, reps):
+        for _ in range(3):
+            fn()
+        barrier()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        barrier()
+        return max_ms(a.elapsed_time(b) / reps)
+
     clk = Clocks(local).__enter__()
     for _ in range(args.warmup):
         step()
-    torch.cuda.synchronize()
     barrier()
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     a.record(stream)
     for _ in range(args.steps):
         step()
     b.record(stream)
-    torch.cuda.synchronize()
     barrier()
-    clk.__exit__()
     ms = max_ms(a.elapsed_time(b) / args.steps)
     D_glob = 2 * int(np.prod([c + 1 for c in counts]))
     value = 2 * D_glob / (ms * 1e-3) / 1e6
+    # residual tile roofline on this rank's slab (32 B/DoF over the CUDA-event
+    # time, max over ranks), HBM peak from MEASURED_PEAKS.json
+    t_res = timed(lambda: res.device_call(u, check=False), max(args.steps, 20))
+    clk.__exit__()
+    hbm_peak, peak_src = hbm_peak_gbs()
+    D_loc = 2 * sum(nlocs)
+    ach = 32 * D_loc / (t_res * 1e-3) / 1e9
+    roofline = {"bound": "hbm", "achieved": round(ach, 1), "peak": hbm_peak, "unit": "GB/s",
+                "frac": round(ach / hbm_peak, 4), "traffic": None, "algorithmic_bytes": 32 * D_loc,
+                "kernel": roofline_kernel_name(w), "bytes_per_dof": 32, "ms_per_launch": round(t_res, 4),
+                "peak_source": peak_src,
+                "note": "per rank (its slab incl. halo exchange), slowest rank; fp64-issue-bound kernel"}
 
     # end to end through the slab API with this rank's host buffers: upload
     # u, v from pinned memory, residual + Jv, download F and Jv, every step
@@ -325,37 +351,95 @@ def run_slabs(args, w, rank, world, local, dist, emulate=0):
             f_pin[i].copy_(f.parts[i], non_blocking=True)
             j_pin[i].copy_(jv.parts[i], non_blocking=True)
 
-    for _ in range(args.warmup):
-        e2e_step()
-    torch.cuda.synchronize()
-    barrier()
-    a.record(stream)
-    for _ in range(args.steps):
-        e2e_step()
-    b.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    e2e_ms = max_ms(a.elapsed_time(b) / args.steps)
+    e2e_ms = timed(e2e_step, args.steps)
     nb = 2 * 2 * sum(nlocs) * 8
     e2e = {"value": round(2 * D_glob / (e2e_ms * 1e-3) / 1e6, 2), "unit": "MDoF/s",
            "h2d_bytes_per_step": nb, "d2h_bytes_per_step": nb,
            "ms_per_step": round(e2e_ms, 3), "note": "per rank (its slabs), max over ranks"}
+    del u_pin, v_pin, f_pin, j_pin, u_d, v_d
+    u = v = old = prev = res = None
+    torch.cuda.empty_cache()
+
+    # seconds per Newton iteration: first (backward-Euler) step of the seeded
+    # dendrite on the same slabs, multicolor V-cycle, NCCL halos + allreduces
+    newton = None
+    if not args.no_newton and w["model"] == "free_growth":
+        st = sp.wrap([seed_initial_condition_device(mesh, kern.params, ctx=c) for c in grp.ctxs])
+        sc0 = uc.ThetaScheme(1.0, w["dt"], 0)
+        walls, rep, t_build = [], None, 0.0
+        for _ in range(4):  # cold + three warm solves (median: host jitter)
+            barrier()
+            t0 = time.perf_counter()
+            pc = SlabPrecond(grp, st, sc0, uc.PrecondConfig(ordering="multicolor"))
+            barrier()
+            t_build = time.perf_counter() - t0
+            r0 = SlabResidual(grp, st, st, sc0)
+            barrier()
+            t0 = time.perf_counter()
+            _, rep = uc.newton_solve(r0, st, uc.NewtonConfig(), precond_apply=pc.apply)
+            barrier()
+            walls.append(max_ms(time.perf_counter() - t0))
+        t_newton = float(np.median(walls[1:]))
+        vv = sp.wrap([torch.randn_like(p) for p in st.parts])
+        t_apply = timed(lambda: pc._uc_deferred(vv), 5)
+        newton = {"sec_per_newton_iteration": round(t_newton / max(rep.iterations, 1), 5),
+                  "newton_iterations": rep.iterations, "gmres_per_newton": rep.gmres_iterations,
+                  "converged": bool(rep.converged), "precond_build_s": round(t_build, 4),
+                  "cold_sec_per_newton_iteration": round(walls[0] / max(rep.iterations, 1), 5),
+                  "vcycle_apply_ms": round(t_apply, 3),
+                  "case": "seed IC, step 0 (backward-Euler startup), default solver settings, slabs",
+                  "ordering": "multicolor", "timing": "host wall clock per solve, max over ranks"}
+        pc = r0 = None
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        cpu = cpu_baseline_line(w)
+    if dist is not None:
+        dist.barrier()
     if rank == 0:
         line = {
             "metric": "MDoF/s residual+Jv fill", "value": round(value, 2), "unit": "MDoF/s",
             "n_gpus": 1 if emulate else world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": round(ms, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": args.workload, "model": w["model"], "dim": w["dim"], "counts": counts,
                        "dof": D_glob, "dof_per_step": 2 * D_glob,
                        "parallelism": (f"slab x{nslab} emulated in one process (testing)" if emulate
                                        else f"slab x{world} (NCCL ghost planes + allreduce)"),
                        "l2": "per-rank inputs larger than L2; no flush"},
-            "gpu_launches": 5 * args.steps, "clocks": clk.summary(), "roofline": None,
-            "e2e": e2e, "cpu_baseline": None,
+            "gpu_launches": 5 * args.steps, "clocks": clk.summary(), "roofline": roofline,
+            "e2e": e2e, "cpu_baseline": cpu, "newton": newton,
         }
         print(json.dumps(line), flush=True)
+
+
+def hbm_peak_gbs():
+    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pk):
+        with open(pk) as fh:
+            peaks = json.load(fh)
+        if "hbm_gbs" in peaks:
+            return float(peaks["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def roofline_kernel_name(w):
+    return f"k_residual<{w['dim']},{'FG' if w['model'] == 'free_growth' else 'ALLOY'},NEW>"
+
+
+def cpu_baseline_line(w):
+    """The CPU port of the reference on this host's cores, bounded sample."""
+    N = int(np.prod([c + 1 for c in w["counts"]]))
+    try:
+        sec, Dc, sample, cores = cpu_oracle_step_time(w, steps=1, warmup=1,
+                                                     rows=None if w["dim"] == 2 and N <= 2049 ** 2 else 128,
+                                                     min_seconds=10.0)
+        return {"value": round(2 * Dc / sec / 1e6, 4), "unit": "MDoF/s", "cores": cores,
+                "kind": "port", "sample": sample + "; residual+Jv of oracle/uc_oracle.c (OpenMP, "
+                                                   f"{cores}-thread C port of the reference)"}
+    except Exception as exc:  # reported, not fatal
+        return {"value": None, "unit": "MDoF/s", "cores": 0, "kind": "port", "sample": f"failed: {exc}"}
 
 
 def main():
@@ -370,17 +454,34 @@ def main():
                     help="testing: run the N>1 slab path with K slabs in this process on one GPU")
     ap.add_argument("--no-newton", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the al2d_4096 / fg3d_256 extra lines")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak = mesh grows with N (default), strong = the named mesh split N ways")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
     w = WORKLOADS[args.workload]
 
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1 and args.impl != "reference":
+        # one rank per GPU: launch them ourselves (the driver's torchrun form)
+        import socket
+
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        sys.exit(subprocess.call(cmd))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, w, rank, world)
         return
+    if "WORLD_SIZE" in os.environ and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}", file=sys.stderr)
+        sys.exit(2)
 
     import torch
 
@@ -397,13 +498,38 @@ def main():
         dist.destroy_process_group()
         return
 
+    line = run_single(args, w, local)
+    print(json.dumps(line), flush=True)
+
+
+def _timed(fn, reps, stream):
+    import torch
+
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(reps):
+        fn()
+    b.record(stream)
+    torch.cuda.synchronize()
+    return a.elapsed_time(b) / reps
+
+
+def fill_phase(args, wname, local, steps, warmup, e2e=True):
+    """Residual + fused Jv on synthetic states of workload `wname`: device-
+    resident throughput, per-kernel times, roofline, end-to-end through the
+    public API with host buffers."""
     import ctypes as C
+
+    import torch
 
     import paper_2006_16764_b200 as uc
     from paper_2006_16764_b200 import _lib as L
     from paper_2006_16764_b200 import device as D
-    from paper_2006_16764_b200.models import seed_initial_condition_device
 
+    w = WORKLOADS[wname]
     dev = torch.device("cuda", local)
     N, u_h, old_h, prev_h, v_h = synthetic_states(w)
     Dof = 2 * N
@@ -412,8 +538,7 @@ def main():
     sc = uc.ThetaScheme(w["theta"], w["dt"], w["step"])
     u = torch.from_numpy(u_h).to(dev)
     v = torch.from_numpy(v_h).to(dev)
-    res = uc.TimestepResidual(mesh, kern, torch.from_numpy(old_h).to(dev),
-                              torch.from_numpy(prev_h).to(dev), sc)
+    res = uc.TimestepResidual(mesh, kern, torch.from_numpy(old_h).to(dev), torch.from_numpy(prev_h).to(dev), sc)
     unorm = D.norm(u)
     stream = torch.cuda.current_stream()
 
@@ -421,80 +546,45 @@ def main():
         f = res.device_call(u, check=False)
         return res.jv_device(u, f, v, unorm)
 
-    def barrier():
-        torch.cuda.synchronize()
-        if dist is not None:
-            dist.barrier()
-
-    def max_over_ranks(x):
-        if dist is None:
-            return x
-        t = torch.tensor([x], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
-
-    # ---- device-resident throughput ------------------------------------
     clk = Clocks(local).__enter__()  # sampled from warm-up through the kernel timings
-    for _ in range(args.warmup):
+    for _ in range(warmup):
         step()
-    barrier()
+    torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    for _ in range(args.steps):
+    for _ in range(steps):
         step()
     ev1.record(stream)
     torch.cuda.synchronize()
-    barrier()
-    ms = max_over_ranks(ev0.elapsed_time(ev1) / args.steps)
-    value = world * 2 * Dof / (ms * 1e-3) / 1e6
+    ms = ev0.elapsed_time(ev1) / steps
+    value = 2 * Dof / (ms * 1e-3) / 1e6
     if res.ctx.status().residual_nonfinite:
         raise RuntimeError("non-finite residual in benchmark inputs")
-
-    # ---- per-kernel durations (CUDA events on the launching stream) ----
-    def timed(fn, reps):
-        for _ in range(3):
-            fn()
-        torch.cuda.synchronize()
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        for _ in range(reps):
-            fn()
-        b.record(stream)
-        torch.cuda.synchronize()
-        return a.elapsed_time(b) / reps
-
     f0 = res.device_call(u, check=False)
-    t_res = timed(lambda: res.device_call(u, check=False), max(args.steps, 50))
-    t_jv = timed(lambda: res.jv_device(u, f0, v, unorm), max(args.steps, 50))
+    t_res = _timed(lambda: res.device_call(u, check=False), max(steps, 50), stream)
+    t_jv = _timed(lambda: res.jv_device(u, f0, v, unorm), max(steps, 50), stream)
     clk.__exit__()
-    peaks = {}
-    pk = os.path.join(ROOT, "MEASURED_PEAKS.json")
-    if os.path.exists(pk):
-        with open(pk) as fh:
-            peaks = json.load(fh)
-    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
-    def roofline_kernel_name(w):
-        return f"k_residual<{w['dim']},{'FG' if w['model'] == 'free_growth' else 'ALLOY'},NEW>"
-
+    hbm_peak, peak_src = hbm_peak_gbs()
     res_bytes = 32 * Dof
     achieved = res_bytes / (t_res * 1e-3) / 1e9
     # DRAM bytes per launch of this kernel from the committed ncu --set full
-    # capture (profiles/r01/ncu_traffic.json), when it covers this workload
+    # capture (profiles/*/ncu_traffic.json, newest round first)
     traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "r01", "ncu_traffic.json")) as fh:
-            traffic = json.load(fh)["kernels"].get(roofline_kernel_name(w), {}).get(args.workload)
-    except (OSError, ValueError, KeyError):
-        traffic = None
+    for rnd in ("r02", "r01"):
+        try:
+            with open(os.path.join(ROOT, "profiles", rnd, "ncu_traffic.json")) as fh:
+                traffic = json.load(fh)["kernels"].get(roofline_kernel_name(w), {}).get(wname)
+        except (OSError, ValueError, KeyError):
+            traffic = None
+        if traffic is not None:
+            break
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_peak, "unit": "GB/s",
-                "frac": round(achieved / hbm_peak, 4), "traffic": traffic,
-                "algorithmic_bytes": res_bytes,
-                "kernel": f"k_residual<{w['dim']},{'FG' if w['model'] == 'free_growth' else 'ALLOY'},NEW>",
-                "bytes_per_dof": 32, "ms_per_launch": round(t_res, 4), "peak_source": peak_src,
+                "frac": round(achieved / hbm_peak, 4), "traffic": traffic, "algorithmic_bytes": res_bytes,
+                "kernel": roofline_kernel_name(w), "bytes_per_dof": 32, "ms_per_launch": round(t_res, 4),
+                "peak_source": peak_src,
                 "note": "fp64-issue-bound kernel; HBM fraction ceiling ~20-30% in 2D (DESIGN.md)"}
     # FP64 roofline of the same kernel: DP instructions per element measured
-    # with ncu (profiles/r01/SUMMARY.md) over the measured DFMA issue rate
+    # with ncu (profiles/dp_inst_per_element.json) over the measured DFMA issue rate
     dp_per_elem = {}
     try:
         with open(os.path.join(ROOT, "profiles", "dp_inst_per_element.json")) as fh:
@@ -521,174 +611,202 @@ def main():
                "residual_mdofs": round(Dof / (t_res * 1e-3) / 1e6, 1),
                "jv_mdofs": round(Dof / (t_jv * 1e-3) / 1e6, 1),
                "jv_gbs": round(48 * Dof / (t_jv * 1e-3) / 1e9, 1)}
+    out = {"value": round(value, 2), "ms_per_step": round(ms, 4), "dof": Dof, "roofline": roofline,
+           "fp64_roofline": fp64, "kernels": kernels, "clocks": clk.summary(),
+           "gpu_launches": 5 * steps}
 
-    # ---- end-to-end through the public API with host buffers ----------
-    # Each step copies u, v from pinned host memory, calls the public API
-    # (TimestepResidual.__call__ + jfnk_matvec) and copies F, Jv back.  Copies
-    # run on two copy streams (double-buffered) so the download of step i
-    # overlaps the upload of step i+1; every byte still moves inside the
-    # timed region.
-    u_pin = torch.from_numpy(u_h).pin_memory()
-    v_pin = torch.from_numpy(v_h).pin_memory()
-    f_pin = [torch.empty(Dof, dtype=torch.float64).pin_memory() for _ in range(2)]
-    j_pin = [torch.empty(Dof, dtype=torch.float64).pin_memory() for _ in range(2)]
-    u_d = [torch.empty(Dof, dtype=torch.float64, device=dev) for _ in range(2)]
-    v_d = [torch.empty(Dof, dtype=torch.float64, device=dev) for _ in range(2)]
-    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-    ev_in = [torch.cuda.Event() for _ in range(2)]
-    ev_out = [torch.cuda.Event() for _ in range(2)]
+    if e2e:
+        # ---- end to end through the public API with host buffers ----------
+        # Each step copies u, v from pinned host memory, calls the public API
+        # (TimestepResidual.__call__ + jfnk_matvec) and copies F, Jv back.  Copies
+        # run on two copy streams (double-buffered) so the download of step i
+        # overlaps the upload of step i+1; every byte still moves inside the
+        # timed region.
+        u_pin = torch.from_numpy(u_h).pin_memory()
+        v_pin = torch.from_numpy(v_h).pin_memory()
+        f_pin = [torch.empty(Dof, dtype=torch.float64).pin_memory() for _ in range(2)]
+        j_pin = [torch.empty(Dof, dtype=torch.float64).pin_memory() for _ in range(2)]
+        u_d = [torch.empty(Dof, dtype=torch.float64, device=dev) for _ in range(2)]
+        v_d = [torch.empty(Dof, dtype=torch.float64, device=dev) for _ in range(2)]
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        ev_in = [torch.cuda.Event() for _ in range(2)]
+        ev_out = [torch.cuda.Event() for _ in range(2)]
 
-    def upload(i):
-        k = i % 2
-        with torch.cuda.stream(s_in):
-            s_in.wait_event(ev_out[k])  # buffer k free again (step i-2's results left)
-            u_d[k].copy_(u_pin, non_blocking=True)
-            v_d[k].copy_(v_pin, non_blocking=True)
-            ev_in[k].record(s_in)
-
-    def e2e_run(nsteps):
-        # the upload of step i+1 is enqueued before step i's API calls (which
-        # synchronise on their non-finite checks), so it overlaps step i's
-        # compute and step i-1's download
-        upload(0)
-        for i in range(nsteps):
+        def upload(i):
             k = i % 2
-            if i + 1 < nsteps:
-                upload(i + 1)
-            stream.wait_event(ev_in[k])
-            F = res(u_d[k])
-            Jv = uc.jfnk_matvec(res, u_d[k], F, v_d[k])
-            ev_out[k].record(stream)
-            with torch.cuda.stream(s_out):
-                s_out.wait_event(ev_out[k])
-                f_pin[k].copy_(F, non_blocking=True)
-                j_pin[k].copy_(Jv, non_blocking=True)
-                ev_out[k].record(s_out)
-            F.record_stream(s_out)  # keep F, Jv alive until their download ran
-            Jv.record_stream(s_out)
+            with torch.cuda.stream(s_in):
+                s_in.wait_event(ev_out[k])  # buffer k free again (step i-2's results left)
+                u_d[k].copy_(u_pin, non_blocking=True)
+                v_d[k].copy_(v_pin, non_blocking=True)
+                ev_in[k].record(s_in)
 
-    e2e_run(args.warmup)
-    torch.cuda.synchronize()
-    barrier()
-    a0, b0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    a0.record(stream)
-    e2e_run(args.steps)
-    stream.wait_stream(s_out)  # end mark after the last download
-    b0.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    e2e_ms = max_over_ranks(a0.elapsed_time(b0) / args.steps)
-    e2e = {"value": round(world * 2 * Dof / (e2e_ms * 1e-3) / 1e6, 2), "unit": "MDoF/s",
-           "h2d_bytes_per_step": 2 * Dof * 8, "d2h_bytes_per_step": 2 * Dof * 8,
-           "ms_per_step": round(e2e_ms, 3), "copies": "pinned, double-buffered copy streams"}
-    launches_per_step = 5  # residual tile + edge fix-up, |v| reduction, Jv tile + edge fix-up
+        def e2e_run(nsteps):
+            # the upload of step i+1 is enqueued before step i's API calls (which
+            # synchronise on their non-finite checks), so it overlaps step i's
+            # compute and step i-1's download
+            upload(0)
+            for i in range(nsteps):
+                k = i % 2
+                if i + 1 < nsteps:
+                    upload(i + 1)
+                stream.wait_event(ev_in[k])
+                F = res(u_d[k])
+                Jv = uc.jfnk_matvec(res, u_d[k], F, v_d[k])
+                ev_out[k].record(stream)
+                with torch.cuda.stream(s_out):
+                    s_out.wait_event(ev_out[k])
+                    f_pin[k].copy_(F, non_blocking=True)
+                    j_pin[k].copy_(Jv, non_blocking=True)
+                    ev_out[k].record(s_out)
+                F.record_stream(s_out)  # keep F, Jv alive until their download ran
+                Jv.record_stream(s_out)
 
-    # ---- Newton step on the seeded dendrite --------------------------
-    # release the fill-phase working set first (512^3: ~2.2 GB per vector)
-    del u_pin, v_pin, f_pin, j_pin, u_d, v_d, f0
-    u = v = res = None
-    import gc
+        e2e_run(warmup)
+        torch.cuda.synchronize()
+        a0, b0 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        e2e_run(steps)
+        stream.wait_stream(s_out)  # end mark after the last download
+        b0.record(stream)
+        torch.cuda.synchronize()
+        e2e_ms = a0.elapsed_time(b0) / steps
+        out["e2e"] = {"value": round(2 * Dof / (e2e_ms * 1e-3) / 1e6, 2), "unit": "MDoF/s",
+                      "h2d_bytes_per_step": 2 * Dof * 8, "d2h_bytes_per_step": 2 * Dof * 8,
+                      "ms_per_step": round(e2e_ms, 3), "copies": "pinned, double-buffered copy streams"}
+    return out
 
-    gc.collect()
-    torch.cuda.empty_cache()
-    free_b, total_b = torch.cuda.mem_get_info()
-    print(f"[bench] device memory before Newton phase: free {free_b / 2**30:.1f} / {total_b / 2**30:.1f} GiB, "
-          f"torch allocated {torch.cuda.memory_allocated() / 2**30:.1f} GiB", file=sys.stderr, flush=True)
-    newton = None
-    if not args.no_newton and w["model"] == "free_growth":
-        u0 = seed_initial_condition_device(mesh, kern.params)
-        if u0 is not None:
-            st = u0
-            sc0 = uc.ThetaScheme(1.0, w["dt"], 0)
-            walls = []
-            pc = r0 = None
-            for rep_i in range(4):  # cold (first) and three warm solves (median: host jitter)
-                pc = r0 = None  # recycle the previous hierarchy (precond._pool)
-                torch.cuda.synchronize()
-                t0 = time.perf_counter()
-                pc = uc.build_precond(mesh, kern, st, sc0, uc.PrecondConfig(ordering="multicolor"))
-                torch.cuda.synchronize()
-                t_build = time.perf_counter() - t0
-                r0 = uc.TimestepResidual(mesh, kern, st, st, sc0)
-                torch.cuda.synchronize()
-                t0 = time.perf_counter()
-                _, rep = uc.newton_solve(r0, st, uc.NewtonConfig(), precond_apply=pc.apply)
-                torch.cuda.synchronize()
-                walls.append(time.perf_counter() - t0)
-            t_newton = float(np.median(walls[1:]))
-            vv = torch.randn_like(st)
-            t_apply = timed(lambda: pc.device_apply(vv, check=False), 5)
+
+def newton_phase(args, wname, orderings=("multicolor",)):
+    """Seconds per implicit Newton iteration: the first (backward-Euler
+    startup) step of the reference's initial condition (free growth: seeded
+    dendrite; alloy: perturbed directional front), default solver settings,
+    cold + three warm solves (median); V-cycle apply time and effective
+    bandwidth; seconds per implicit time step through driver.simulate (the
+    package's time loop)."""
+    import torch
+
+    import paper_2006_16764_b200 as uc
+    from paper_2006_16764_b200.config import default_config
+    from paper_2006_16764_b200.driver import simulate
+    from paper_2006_16764_b200.models import directional_initial_condition_device, seed_initial_condition_device
+
+    w = WORKLOADS[wname]
+    mesh = uc.build_mesh(w["dim"], w["extents"], w["counts"])
+    kern = uc.FreeGrowthKernel() if w["model"] == "free_growth" else uc.AlloyKernel()
+    if w["model"] == "free_growth":
+        st = seed_initial_condition_device(mesh, kern.params)
+    else:
+        st = directional_initial_condition_device(mesh, kern.params, amplitude=0.5, seed=0, smooth=True)
+    sc0 = uc.ThetaScheme(1.0, w["dt"], 0)
+    stream = torch.cuda.current_stream()
+    N = mesh.n_nodes
+    hbm_peak, _ = hbm_peak_gbs()
+    out = {}
+    for ordering in orderings:
+        walls, rep, t_build, pc = [], None, 0.0, None
+        reps = 4 if ordering == "multicolor" else 1
+        clk = Clocks(torch.cuda.current_device()).__enter__()
+        for _ in range(reps):  # cold (first) and warm solves (median: host jitter)
+            pc = None  # recycle the previous hierarchy (precond._pool)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            pc = uc.build_precond(mesh, kern, st, sc0, uc.PrecondConfig(ordering=ordering))
+            torch.cuda.synchronize()
+            t_build = time.perf_counter() - t0
+            r0 = uc.TimestepResidual(mesh, kern, st, st, sc0)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            _, rep = uc.newton_solve(r0, st, uc.NewtonConfig(), precond_apply=pc.apply)
+            torch.cuda.synchronize()
+            walls.append(time.perf_counter() - t0)
+        vv = torch.randn_like(st)
+        t_apply = _timed(lambda: pc.device_apply(vv, check=False), 5 if ordering == "multicolor" else 2, stream)
+        clk.__exit__()
+        t_newton = float(np.median(walls[1:] if len(walls) > 1 else walls))
+        d = {"sec_per_newton_iteration": round(t_newton / max(rep.iterations, 1), 5),
+             "newton_iterations": rep.iterations, "gmres_per_newton": rep.gmres_iterations,
+             "converged": bool(rep.converged), "precond_build_s": round(t_build, 4),
+             "vcycle_apply_ms": round(t_apply, 3), "clocks": clk.summary()}
+        if ordering == "multicolor":
             vb = vcycle_bytes(pc, N, w["dim"])
-            pc = r0 = None
-            # full implicit time steps (precond build + Newton) through the host loop
-            from paper_2006_16764_b200.stepper import run_steps
-            step_walls = []
-            state = st
-            prev_state = st
-            for n in range(3):
-                torch.cuda.synchronize()
-                t0 = time.perf_counter()
-                state_new, recs = run_steps(mesh, kern, state, 1, 0.5, w["dt"], startup_steps=0)
-                torch.cuda.synchronize()
-                step_walls.append(time.perf_counter() - t0)
-                state = state_new
-            newton = {"sec_per_newton_iteration": round(t_newton / max(rep.iterations, 1), 5),
-                      "newton_iterations": rep.iterations, "gmres_per_newton": rep.gmres_iterations,
-                      "converged": bool(rep.converged), "precond_build_s": round(t_build, 4),
-                      "cold_sec_per_newton_iteration": round(walls[0] / max(rep.iterations, 1), 5),
-                      "sec_per_time_step": round(float(np.mean(step_walls[1:])), 5),
-                      "time_step_walls_s": [round(x, 5) for x in step_walls],
-                      "vcycle_apply_ms": round(t_apply, 3),
+            d.update({"cold_sec_per_newton_iteration": round(walls[0] / max(rep.iterations, 1), 5),
                       "vcycle_gbs": round(vb / (t_apply * 1e-3) / 1e9, 1),
                       "vcycle_hbm_frac": round(vb / (t_apply * 1e-3) / 1e9 / hbm_peak, 4),
-                      "case": "seed IC, step 0 (backward-Euler startup), default solver settings",
-                      "ordering": "multicolor"}
-            # the reference's DEFAULT smoother ordering: exact sequential
-            # (lexicographic) Gauss-Seidel, pipelined wavefront kernel
-            if not args.no_lex and N <= 2049 * 2049:
-                pc = uc.build_precond(mesh, kern, st, sc0, uc.PrecondConfig(ordering="lexicographic"))
-                r0 = uc.TimestepResidual(mesh, kern, st, st, sc0)
-                torch.cuda.synchronize()
-                t0 = time.perf_counter()
-                _, rep_l = uc.newton_solve(r0, st, uc.NewtonConfig(), precond_apply=pc.apply)
-                torch.cuda.synchronize()
-                t_lex = time.perf_counter() - t0
-                t_apply_l = timed(lambda: pc.device_apply(vv, check=False), 3)
-                pc = r0 = None
-                newton["lexicographic"] = {
-                    "sec_per_newton_iteration": round(t_lex / max(rep_l.iterations, 1), 5),
-                    "newton_iterations": rep_l.iterations, "gmres_per_newton": rep_l.gmres_iterations,
-                    "vcycle_apply_ms": round(t_apply_l, 3),
-                    "note": "reference default ordering; sequential sweep as a pipelined wavefront (fronts i+2j)"}
+                      "case": ("seed IC" if w["model"] == "free_growth" else "directional IC (amplitude 0.5)")
+                              + ", step 0 (backward-Euler startup), default solver settings",
+                      "ordering": "multicolor"})
+            out.update(d)
+        else:
+            d["note"] = "the reference's default ordering: exact sequential sweep (pipelined wavefront)"
+            out[ordering] = d
+        pc = r0 = None
+    # implicit time steps through the package's time loop (driver.simulate):
+    # startup step(s) then Crank-Nicolson, preconditioner rebuilt every step
+    cfg = default_config(w["model"])
+    cfg.mesh.dimension, cfg.mesh.extents, cfg.mesh.counts = w["dim"], tuple(w["extents"]), tuple(w["counts"])
+    cfg.time.dt = w["dt"]
+    cfg.time.t_final = 3 * w["dt"]
+    cfg.precond.ordering = "multicolor"
+    res = simulate(cfg)
+    out["sec_per_time_step"] = round(res.loop_seconds / max(res.steps_completed, 1), 5)
+    out["time_steps"] = {"steps": res.steps_completed, "newton": [r["newton_iters"] for r in res.records],
+                         "gmres": [r["gmres_iters"] for r in res.records], "status": res.status,
+                         "loop": "driver.simulate (startup step at theta=1, then theta=0.5)"}
+    return out
 
+
+def run_single(args, w, local):
+    import gc
+
+    import torch
+
+    torch.cuda.set_device(local)
+    fill = fill_phase(args, args.workload, local, args.steps, args.warmup)
+    gc.collect()
+    torch.cuda.empty_cache()
+    newton = None
+    if not args.no_newton:
+        orderings = ("multicolor",)
+        if not args.no_lex and w["dim"] == 2 and np.prod(w["counts"]) <= 2048 * 2048:
+            orderings = ("multicolor", "lexicographic")
+        newton = newton_phase(args, args.workload, orderings)
+        gc.collect()
+        torch.cuda.empty_cache()
+    # the other named configs (BASELINE.json configs[2], configs[3]) on this GPU:
+    # fill + seconds per Newton iteration, each with its clock record
+    extra = {}
+    if not args.no_extra and args.workload == "fg2d_2048":
+        for wname in ("al2d_4096", "fg3d_256"):
+            try:
+                ex = fill_phase(args, wname, local, max(args.steps // 2, 5), args.warmup, e2e=False)
+                gc.collect()
+                torch.cuda.empty_cache()
+                if not args.no_newton:
+                    ex["newton"] = newton_phase(args, wname)
+                ex["config"] = {k: WORKLOADS[wname][k] for k in ("model", "dim", "counts")}
+                extra[wname] = ex
+            except Exception as exc:  # reported, never fatal to the headline line
+                extra[wname] = {"error": repr(exc)}
+            gc.collect()
+            torch.cuda.empty_cache()
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        try:
-            sec, Dc, sample, cores = cpu_oracle_step_time(w, steps=1, warmup=1,
-                                                         rows=None if w["dim"] == 2 and N <= 2049 ** 2 else 128,
-                                                         min_seconds=10.0)
-            cpu = {"value": round(2 * Dc / sec / 1e6, 4), "unit": "MDoF/s", "cores": cores,
-                   "kind": "port", "sample": sample + "; residual+Jv of oracle/uc_oracle.c (OpenMP)"}
-        except Exception as exc:  # reported, not fatal
-            cpu = {"value": None, "unit": "MDoF/s", "cores": 0, "kind": "port", "sample": f"failed: {exc}"}
-
-    if rank == 0:
-        line = {
-            "metric": "MDoF/s residual+Jv fill", "value": round(value, 2), "unit": "MDoF/s",
-            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": round(ms, 4), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": args.workload, "model": w["model"], "dim": w["dim"],
-                       "counts": list(w["counts"]), "dof": Dof, "dof_per_step": 2 * Dof,
-                       "l2": "inputs (~470 MB working set) larger than L2; no flush",
-                       "parallelism": f"replicas x{world}"},
-            "roofline": roofline, "fp64_roofline": fp64, "kernels": kernels, "e2e": e2e,
-            "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(),
-            "newton": newton, "cpu_baseline": cpu,
-        }
-        print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.destroy_process_group()
+    if not args.no_cpu_baseline:
+        cpu = cpu_baseline_line(w)
+    Dof = fill["dof"]
+    line = {
+        "metric": "MDoF/s residual+Jv fill", "value": fill["value"], "unit": "MDoF/s",
+        "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": fill["ms_per_step"], "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.workload, "model": w["model"], "dim": w["dim"],
+                   "counts": list(w["counts"]), "dof": Dof, "dof_per_step": 2 * Dof,
+                   "l2": "inputs (~470 MB working set) larger than L2; no flush",
+                   "parallelism": "single GPU"},
+        "roofline": fill["roofline"], "fp64_roofline": fill["fp64_roofline"], "kernels": fill["kernels"],
+        "e2e": fill["e2e"], "gpu_launches": fill["gpu_launches"], "clocks": fill["clocks"],
+        "newton": newton, "workloads": extra or None, "cpu_baseline": cpu,
+    }
+    return line
 
 
 if __name__ == "__main__":

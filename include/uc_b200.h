@@ -206,6 +206,28 @@ int uc_sub(uc_ctx* ctx, int64_t n, const double* a, const double* b, double* out
 int uc_scale_div(uc_ctx* ctx, int64_t n, const double* a, double s, double* out);
 /* out = s * a */
 int uc_scale(uc_ctx* ctx, int64_t n, double s, const double* a, double* out);
+/* frozen_quad_state (undercool/assembly.py:193-211, _interp :111-116,
+ * gauss_coords mesh.py:119-128) of a whole mesh: for every element e and
+ * quadrature point q of the rule, vals[f][e][q], grads[f][d][e][q] and
+ * coords[e][q][d] (coords may be NULL).  tables = [values nq x nloc |
+ * physical gradients nq x nloc x dim | jxw nq | reference points nq x dim]
+ * (mesh.py:151-176) on the device. */
+int uc_quad_state(uc_ctx* ctx, const double* state, int nfields, const double* tables, int nq,
+                  double* coords, double* vals, double* grads);
+/* assemble_field_matrix (assembly.py:271-303): (cmass psi_j, psi_i) +
+ * (cdiff grad psi_j, grad psi_i) in CSR (n_nodes + 1 row pointers, int32
+ * column indices sorted per row, one entry per element coupling, duplicates
+ * summed).  cmass/cdiff: per (element, quadrature point) with stride nq, or
+ * one scalar with stride 0.  uc_field_matrix_nnz gives the entry count. */
+int64_t uc_field_matrix_nnz(uc_ctx* ctx);
+int uc_field_matrix(uc_ctx* ctx, const double* cmass, int64_t cmass_stride, const double* cdiff,
+                    int64_t cdiff_stride, const double* tables, int nq, int64_t* indptr, int32_t* indices,
+                    double* data);
+
+/* Host-visible vector tests of the Newton control flow (newton.py:144,175-176
+ * np.all(np.isfinite(x)), np.any(x)): *nonfinite = 1 if some entry is NaN/Inf,
+ * *nonzero = 1 if some entry is non-zero.  Synchronises the context stream. */
+int uc_vec_check(uc_ctx* ctx, int64_t n, const double* a, int32_t* nonfinite, int32_t* nonzero);
 
 /* build_precond (precond.py:269-299): frozen Gauss-point state -> block
  * coefficients (free_growth.py:223-231 / alloy.py:286-300) -> fixed 9/27-point
@@ -301,6 +323,27 @@ int uc_nccl_unique_id(const char* nccl_path, void* out128);
 int uc_comm_init_nccl(const char* nccl_path, const void* id128, int rank, int nranks);
 int uc_comm_finalize(void);
 int uc_ctx_set_neighbors(uc_ctx* ctx, int lo_rank, int hi_rank);
+
+/* Host-staged transport: the same remote branches of the exchange and global
+ * sums (csrc/comm.cu) with the planes and partial sums staged through pinned
+ * host buffers and moved by caller-supplied callbacks (e.g. torch.distributed
+ * over gloo).  For testing the multi-rank code path where NCCL cannot run
+ * (several ranks sharing one GPU); every call synchronises the stream.
+ *   sendrecv: perform all ops (kind 0 = send `count` doubles from buf to peer,
+ *             1 = receive into buf from peer) and return 0 on success;
+ *   allreduce_sum: in-place sum of n doubles over all ranks, 0 on success. */
+typedef struct uc_host_op {
+  int32_t kind;
+  int32_t peer;
+  int64_t count;
+  double* buf;
+} uc_host_op;
+typedef struct uc_host_transport {
+  void* user;
+  int (*sendrecv)(void* user, int nops, const uc_host_op* ops);
+  int (*allreduce_sum)(void* user, double* vals, int n);
+} uc_host_transport;
+int uc_comm_init_host(const uc_host_transport* transport, int rank, int nranks);
 int uc_ctx_link_local(uc_ctx* lower, uc_ctx* upper);
 
 int uc_residual_group(uc_ctx* const* ctxs, int n, const uc_scheme* sc, int part,

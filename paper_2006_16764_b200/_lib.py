@@ -43,6 +43,18 @@ class PrecondCfg(C.Structure):
                 ("levels", C.c_int32), ("coarse_sweeps", C.c_int32), ("ordering", C.c_int32)]
 
 
+class HostOp(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("peer", C.c_int32), ("count", C.c_int64), ("buf", C.POINTER(C.c_double))]
+
+
+SENDRECV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int, C.POINTER(HostOp))
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_int)
+
+
+class HostTransport(C.Structure):
+    _fields_ = [("user", C.c_void_p), ("sendrecv", SENDRECV_FN), ("allreduce_sum", ALLREDUCE_FN)]
+
+
 class DiagArgs(C.Structure):
     _fields_ = [("what", C.c_int32), ("pad", C.c_int32), ("elem_node_weight", C.c_double * 8),
                 ("composition", C.c_double), ("tip_level", C.c_double), ("extent_x", C.c_double)]
@@ -85,6 +97,10 @@ SIGNATURES = {
     "uc_sub": (_I, [_P, _I64, _P, _P, _P]),
     "uc_scale_div": (_I, [_P, _I64, _P, _D, _P]),
     "uc_scale": (_I, [_P, _I64, _D, _P, _P]),
+    "uc_quad_state": (_I, [_P, _P, _I, _P, _I, _P, _P, _P]),
+    "uc_field_matrix_nnz": (_I64, [_P]),
+    "uc_field_matrix": (_I, [_P, _P, _I64, _P, _I64, _P, _I, _P, _P, _P]),
+    "uc_vec_check": (_I, [_P, _I64, _P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     "uc_precond_build": (_I, [_P, C.POINTER(Scheme), _P, C.POINTER(PrecondCfg)]),
     "uc_precond_apply": (_I, [_P, _P, _P]),
     "uc_precond_stencil": (_I, [_P, _I, _I, _P]),
@@ -102,6 +118,7 @@ SIGNATURES = {
     "uc_nccl_unique_id": (_I, [C.c_char_p, _P]),
     "uc_comm_init_nccl": (_I, [C.c_char_p, _P, _I, _I]),
     "uc_comm_finalize": (_I, []),
+    "uc_comm_init_host": (_I, [C.POINTER(HostTransport), _I, _I]),
     "uc_ctx_set_neighbors": (_I, [_P, _I, _I]),
     "uc_ctx_link_local": (_I, [_P, _P]),
     "uc_residual_group": (_I, [C.POINTER(_P), _I, C.POINTER(Scheme), _I] + [C.POINTER(_P)] * 5),

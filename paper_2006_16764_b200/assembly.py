@@ -23,8 +23,9 @@ from .device import as_device, context_for, is_device, to_host
 from .errors import NonFiniteResidualError
 from .models import n_fields_of
 
-__all__ = ["StateHistory", "split_fields", "join_fields", "assemble_residual",
-           "TimestepResidual", "NonFiniteResidualError", "scheme_struct"]
+__all__ = ["StateHistory", "QuadState", "split_fields", "join_fields", "assemble_residual",
+           "TimestepResidual", "NonFiniteResidualError", "scheme_struct", "frozen_quad_state",
+           "assemble_field_matrix"]
 
 
 @dataclass
@@ -32,6 +33,25 @@ class StateHistory:
     new: object
     old: object
     prev: object
+
+
+@dataclass
+class QuadState:
+    """Fields at quadrature points (assembly.py:57-75): ``val_*[f]`` is
+    (n_elem, nq), ``grad_*[f]`` a dim-tuple of (n_elem, nq) components,
+    ``coords`` (n_elem, nq, dim).  Device arrays when the state was a CUDA
+    tensor, numpy otherwise."""
+
+    part: str
+    t_new: float
+    t_old: float
+    coords: object = None
+    val_new: list | None = None
+    grad_new: list | None = None
+    val_old: list | None = None
+    grad_old: list | None = None
+    rate0: object = None
+    val0_old: object = None
 
 
 def split_fields(u, n_fields: int):
@@ -255,3 +275,82 @@ def _raise_nonfinite_subset(ctx, sc, part, u, old, prev, mask, ids, mesh):
     raise NonFiniteResidualError(
         f"non-finite {name} integrand for field {f} at element {pos} "
         f"(first node {first}), quadrature point {q}")
+
+
+def _basis_tables(mesh, rule):
+    """Device copy of the rule's basis tables [V | G | jxw | points] (mesh.py:151-176)."""
+    from .mesh import _as_rule
+
+    if int(getattr(mesh, "order", 1)) != 1:
+        raise NotImplementedError("only Q1 meshes run on the B200 path")
+    r = _as_rule(rule) if rule is not None else None
+    b = mesh.basis(r) if hasattr(mesh, "basis") else None
+    if b is None or r is None:
+        from .mesh import gauss_rule, _tabulate_basis
+
+        r = r or gauss_rule(mesh.dim)
+        b = _tabulate_basis(mesh, r)
+    flat = np.concatenate([b.values.reshape(-1), b.gradients.reshape(-1), b.jxw.reshape(-1),
+                           r.points.reshape(-1)])
+    return torch.tensor(flat, dtype=torch.float64, device="cuda"), r.n_points
+
+
+def frozen_quad_state(mesh, kernel, state, scheme, rule=None) -> QuadState:
+    """One state interpolated to the quadrature points (assembly.py:193-211):
+    values, physical gradients and point coordinates of every element, on the
+    device (k_quad_state, any tensor Gauss rule).  Whole meshes only."""
+    nf = n_fields_of(kernel)
+    host = not is_device(state)
+    u = as_device(state)
+    ctx = context_for(mesh, kernel)
+    tables, nq = _basis_tables(mesh, rule)
+    ne, dim = mesh.n_elements, mesh.dim
+    vals = torch.empty((nf, ne, nq), dtype=torch.float64, device=u.device)
+    grads = torch.empty((nf, dim, ne, nq), dtype=torch.float64, device=u.device)
+    coords = torch.empty((ne, nq, dim), dtype=torch.float64, device=u.device)
+    L.check(ctx.lib.uc_quad_state(ctx.bind(), L.ptr(u), nf, L.ptr(tables), nq, L.ptr(coords), L.ptr(vals),
+                                  L.ptr(grads)), "uc_quad_state")
+    cv = (lambda t: to_host(t)) if host else (lambda t: t)
+    qs = QuadState(part="new", t_new=scheme.t_new, t_old=scheme.t_old)
+    qs.coords = cv(coords)
+    qs.val_new = [cv(vals[f]) for f in range(nf)]
+    qs.grad_new = [tuple(cv(grads[f, d]) for d in range(dim)) for f in range(nf)]
+    return qs
+
+
+def assemble_field_matrix(mesh, cmass, cdiff, rule=None):
+    """(cmass psi_j, psi_i) + (cdiff grad psi_j, grad psi_i) (assembly.py:271-303)
+    on the device, written straight into CSR (k_field_csr).  cmass/cdiff are
+    scalars or (n_elements, nq) arrays; numpy/scalar coefficients give a
+    scipy.sparse.csr_matrix (as the reference), CUDA tensors a torch sparse CSR
+    tensor on the device.  Whole Q1 meshes only."""
+    from .models import FreeGrowthKernel
+
+    tables, nq = _basis_tables(mesh, rule)
+    ne = mesh.n_elements
+    on_device = any(isinstance(c, torch.Tensor) and c.is_cuda for c in (cmass, cdiff))
+
+    def coef(c):
+        t = c if isinstance(c, torch.Tensor) else torch.as_tensor(np.asarray(c, dtype=float))
+        t = t.to(device="cuda", dtype=torch.float64).contiguous()
+        if t.dim() == 0 or t.numel() == 1:
+            return t.reshape(1), 0
+        if tuple(t.shape) != (ne, nq):
+            raise ValueError(f"coefficient shape {tuple(t.shape)} is not (n_elements, nq) = ({ne}, {nq})")
+        return t, nq
+
+    cm, cms = coef(cmass)
+    cd, cds = coef(cdiff)
+    ctx = context_for(mesh, FreeGrowthKernel())
+    nnz = int(ctx.lib.uc_field_matrix_nnz(ctx.bind()))
+    n = mesh.n_nodes
+    indptr = torch.empty(n + 1, dtype=torch.int64, device="cuda")
+    indices = torch.empty(nnz, dtype=torch.int32, device="cuda")
+    data = torch.empty(nnz, dtype=torch.float64, device="cuda")
+    L.check(ctx.lib.uc_field_matrix(ctx.bind(), L.ptr(cm), cms, L.ptr(cd), cds, L.ptr(tables), nq, L.ptr(indptr),
+                                    L.ptr(indices), L.ptr(data)), "uc_field_matrix")
+    if on_device:
+        return torch.sparse_csr_tensor(indptr, indices.to(torch.int64), data, size=(n, n))
+    import scipy.sparse as sps
+
+    return sps.csr_matrix((to_host(data), to_host(indices), to_host(indptr)), shape=(n, n))

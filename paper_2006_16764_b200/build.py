@@ -40,15 +40,30 @@ def _deps():
         glob.glob(os.path.join(CSRC, "*.h"))) + [os.path.join(ROOT, "include", "uc_b200.h")]
 
 
-def stale() -> bool:
+STAMP = LIB + ".flags"
+
+
+def _flags_key(extra) -> str:
+    return " ".join(ARCH + FLAGS + list(extra or []))
+
+
+def stale(extra=None) -> bool:
+    """Sources newer than the library, or the library was built with other
+    compile flags (e.g. an A/B variant from tools/gpu_ab*.sh)."""
     if not os.path.exists(LIB):
+        return True
+    try:
+        with open(STAMP) as fh:
+            if fh.read() != _flags_key(extra):
+                return True
+    except OSError:
         return True
     t = os.path.getmtime(LIB)
     return any(os.path.getmtime(p) > t for p in _deps())
 
 
 def build(force: bool = False, verbose: bool = False, extra=None) -> str:
-    if not force and not stale():
+    if not force and not stale(extra):
         return LIB
     os.makedirs(OUTDIR, exist_ok=True)
     objdir = os.path.join(OUTDIR, "obj")
@@ -81,6 +96,8 @@ def build(force: bool = False, verbose: bool = False, extra=None) -> str:
     if r.returncode != 0:
         raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, LIB)
+    with open(STAMP, "w") as fh:
+        fh.write(_flags_key(extra))
     return LIB
 
 

@@ -239,7 +239,7 @@ int uc_jv_group(uc_ctx* const* ctxs, int n, const uc_scheme* sc, const double* c
   std::vector<double*> vn(n);
   const bool sum = group_needs_sum(G);
   for (int i = 0; i < n; ++i) {
-    vn[i] = G[i]->scal + (UC_SCAL_SLOTS - 1);
+    vn[i] = G[i]->scal + (G[i]->scal_cap - 1);
     if ((rc = reduce_dot(G[i], vec_len(G[i]), v[i], nullptr, vn[i], !sum))) return rc;
   }
   if (sum && (rc = global_sum(G, vn.data(), true, s))) return rc;
@@ -265,7 +265,7 @@ int uc_dot_group(uc_ctx* const* ctxs, int n, const double* const* a, const doubl
   std::vector<double*> slot(n);
   int rc;
   for (int i = 0; i < n; ++i) {
-    slot[i] = G[i]->scal + (UC_SCAL_SLOTS - 2);
+    slot[i] = G[i]->scal + (G[i]->scal_cap - 2);
     if ((rc = reduce_dot(G[i], vec_len(G[i]), a[i], b ? b[i] : nullptr, slot[i], false))) return rc;
   }
   if ((rc = global_sum(G, slot.data(), do_sqrt != 0, s))) return rc;

@@ -153,6 +153,21 @@ __global__ void k_nonfinite(int64_t n, const double* __restrict__ a, unsigned in
   if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) *(volatile unsigned int*)flag = 1u;
 }
 
+// bit 0: some entry is non-finite; bit 1: some entry is non-zero.  One atomic
+// per block into a device word (not the mapped host flags: a per-warp atomic
+// over PCIe costs milliseconds on a full vector).
+__global__ void k_vec_check(int64_t n, const double* __restrict__ a, unsigned int* flag) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  bool bad = false, nz = false;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double v = a[i];
+    bad |= !isfinite(v);
+    nz |= v != 0.0;
+  }
+  const bool anyb = __syncthreads_or(bad), anyz = __syncthreads_or(nz);
+  if (threadIdx.x == 0 && (anyb || anyz)) atomicOr(flag, (anyb ? 1u : 0u) | (anyz ? 2u : 0u));
+}
+
 static inline unsigned ew_grid(uc_ctx* c, int64_t n) {
   int64_t b = (n + 255) / 256;
   const int64_t cap = (int64_t)c->num_sms * 16;
@@ -164,6 +179,28 @@ static inline unsigned ew_grid(uc_ctx* c, int64_t n) {
 int launch_axpy(uc_ctx* c, int64_t n, const double* a, double s, const double* b, double* out) {
   k_axpy<<<ew_grid(c, n), 256, 0, c->stream>>>(n, a, s, b, out, 0);
   UC_CUDA_OK(cudaGetLastError());
+  return UC_OK;
+}
+
+int ensure_scal(uc_ctx* c, int64_t need) {
+  need += 3;  // the fixed slots at the end (api.cu: |v| of uc_jv_group, dot results; uc_vec_check)
+  if (need <= c->scal_cap) return UC_OK;
+  int64_t cap = c->scal_cap;
+  while (cap < need) cap *= 2;
+  UC_CUDA_OK(cudaStreamSynchronize(c->stream));
+  double *d = nullptr, *h = nullptr;
+  UC_CUDA_OK(cudaMalloc(&d, sizeof(double) * cap));
+  UC_CUDA_OK(cudaMemset(d, 0, sizeof(double) * cap));
+  cudaError_t e = cudaMallocHost(&h, sizeof(double) * cap);
+  if (e != cudaSuccess) {
+    cudaFree(d);
+    return set_cuda_error(e, "ensure_scal", __FILE__, __LINE__);
+  }
+  cudaFree(c->scal);
+  cudaFreeHost(c->pinned);
+  c->scal = d;
+  c->pinned = h;
+  c->scal_cap = (int)cap;
   return UC_OK;
 }
 
@@ -185,6 +222,22 @@ int nonfinite_flag_on(cudaStream_t s, int64_t n, const double* a, unsigned int* 
 using namespace uc;
 
 extern "C" {
+
+int uc_vec_check(uc_ctx* c, int64_t n, const double* a, int32_t* nonfinite, int32_t* nonzero) {
+  if (!c || n < 0 || !nonfinite || !nonzero) return set_error(UC_ERR_ARG, "uc_vec_check: bad argument");
+  unsigned int* word = reinterpret_cast<unsigned int*>(c->scal + (c->scal_cap - 3));
+  UC_CUDA_OK(cudaMemsetAsync(word, 0, sizeof(unsigned int), c->stream));
+  if (n > 0) {
+    k_vec_check<<<ew_grid(c, n), 256, 0, c->stream>>>(n, a, word);
+    UC_CUDA_OK(cudaGetLastError());
+  }
+  UC_CUDA_OK(cudaMemcpyAsync(c->pinned, word, sizeof(unsigned int), cudaMemcpyDeviceToHost, c->stream));
+  UC_CUDA_OK(cudaStreamSynchronize(c->stream));
+  const unsigned bits = *reinterpret_cast<volatile unsigned int*>(c->pinned);
+  *nonfinite = (bits & 1u) ? 1 : 0;
+  *nonzero = (bits & 2u) ? 1 : 0;
+  return UC_OK;
+}
 
 int uc_dot(uc_ctx* c, int64_t n, const double* a, const double* b, double* out_dev) {
   if (!c || n < 0) return set_error(UC_ERR_ARG, "uc_dot: bad argument");
@@ -234,7 +287,10 @@ int uc_norm_host(uc_ctx* c, int64_t n, const double* a, double* out) {
 static int arnoldi_group(const Group& G, const int64_t* n, const double* const* const* basis, int k,
                          double* const* w, double scale, double* h_host, int* broke) {
   const int ns = (int)G.size();
-  if (k < 0 || 3 * (k + 2) + 8 > UC_SCAL_SLOTS) return set_error(UC_ERR_ARG, "uc_arnoldi: bad k=%d", k);
+  if (k < 0) return set_error(UC_ERR_ARG, "uc_arnoldi: bad k=%d", k);
+  // any restart length (krylov.py:128-129 has no bound): grow the scalar slots
+  for (uc_ctx* c : G)
+    if (int rc0 = ensure_scal(c, 3 * (int64_t)(k + 2) + 8)) return rc0;
   cudaStream_t s = G[0]->stream;
   const bool sum = group_needs_sum(G);
   // per slab scalar layout: [0, k+2) h; then 2(k+1)+1 dot slots

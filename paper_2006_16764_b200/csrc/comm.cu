@@ -13,6 +13,7 @@
 #include <dlfcn.h>
 
 #include <cstring>
+#include <vector>
 
 #include "uc_internal.h"
 
@@ -38,6 +39,67 @@ struct NcclApi {
 };
 static NcclApi g_nccl;
 static const int kNcclFloat64 = 8, kNcclSum = 0;
+
+// Host-staged transport (uc_comm_init_host): remote sends/receives of one
+// exchange() are collected, staged through pinned host memory and handed to
+// the caller's callbacks in one batch.
+struct HostTransport {
+  bool active = false;
+  uc_host_transport t{};
+  int rank = -1, nranks = 0;
+  double* stage = nullptr;
+  size_t stage_n = 0;
+};
+static HostTransport g_host;
+struct PendingOp {
+  int kind;  // 0 send, 1 recv
+  int peer;
+  int64_t count;
+  const double* src;
+  double* dst;
+};
+
+static int host_stage(size_t n) {
+  if (n <= g_host.stage_n) return UC_OK;
+  if (g_host.stage) cudaFreeHost(g_host.stage);
+  g_host.stage = nullptr;
+  size_t cap = g_host.stage_n ? g_host.stage_n : 1024;
+  while (cap < n) cap *= 2;
+  UC_CUDA_OK(cudaMallocHost(&g_host.stage, sizeof(double) * cap));
+  g_host.stage_n = cap;
+  return UC_OK;
+}
+
+static int host_flush(std::vector<PendingOp>& ops, cudaStream_t s) {
+  if (ops.empty()) return UC_OK;
+  size_t total = 0;
+  for (const PendingOp& o : ops) total += (size_t)o.count;
+  int rc = host_stage(total);
+  if (rc) return rc;
+  std::vector<uc_host_op> hops(ops.size());
+  size_t off = 0;
+  for (size_t i = 0; i < ops.size(); ++i) {
+    hops[i].kind = ops[i].kind;
+    hops[i].peer = ops[i].peer;
+    hops[i].count = ops[i].count;
+    hops[i].buf = g_host.stage + off;
+    if (ops[i].kind == 0)
+      UC_CUDA_OK(cudaMemcpyAsync(hops[i].buf, ops[i].src, sizeof(double) * ops[i].count, cudaMemcpyDeviceToHost, s));
+    off += (size_t)ops[i].count;
+  }
+  UC_CUDA_OK(cudaStreamSynchronize(s));
+  if (g_host.t.sendrecv(g_host.t.user, (int)hops.size(), hops.data()) != 0)
+    return set_error(UC_ERR_CUDA, "host transport: sendrecv callback failed");
+  for (size_t i = 0; i < ops.size(); ++i)
+    if (ops[i].kind == 1)
+      UC_CUDA_OK(cudaMemcpyAsync(ops[i].dst, hops[i].buf, sizeof(double) * ops[i].count, cudaMemcpyHostToDevice, s));
+  // the staging buffer is reused by the next exchange: wait for the uploads
+  UC_CUDA_OK(cudaStreamSynchronize(s));
+  ops.clear();
+  return UC_OK;
+}
+
+bool comm_is_host() { return g_host.active; }
 
 static int nccl_load(const char* path) {
   if (g_nccl.handle) return UC_OK;
@@ -112,10 +174,30 @@ int halo_vectors(const Group& g, int slot, const double* const* vecs, cudaStream
 // plane -> lower neighbour's upper ghost.
 int exchange(const Group& g, const PlaneAddr& addr, bool dir_up, bool dir_down, cudaStream_t s) {
   const bool remote = group_has_remote(g);
+  const bool host = remote && g_host.active;
+  std::vector<PendingOp> pend;
+  auto send = [&](const double* src, int64_t count, int peer) -> int {
+    if (host) {
+      pend.push_back(PendingOp{0, peer, count, src, nullptr});
+      return UC_OK;
+    }
+    UC_NCCL_OK(g_nccl.send(src, count, kNcclFloat64, peer, g_nccl.comm, s));
+    return UC_OK;
+  };
+  auto recv = [&](double* dst, int64_t count, int peer) -> int {
+    if (host) {
+      pend.push_back(PendingOp{1, peer, count, nullptr, dst});
+      return UC_OK;
+    }
+    UC_NCCL_OK(g_nccl.recv(dst, count, kNcclFloat64, peer, g_nccl.comm, s));
+    return UC_OK;
+  };
+  if (remote && !host && !g_nccl.comm) return set_error(UC_ERR_ARG, "remote neighbours but no communicator");
   auto ok = [&addr](int64_t plane) { return !addr.plane_ok || addr.plane_ok(plane); };
   auto lo_of = [&addr](uc_ctx* c) { return addr.slo ? addr.slo(c) : c->grid.lo; };
   auto hi_of = [&addr](uc_ctx* c) { return addr.shi ? addr.shi(c) : c->grid.hi; };
-  if (remote) UC_NCCL_OK(g_nccl.groupStart());
+  if (remote && !host) UC_NCCL_OK(g_nccl.groupStart());
+  int rc = UC_OK;
   for (uc_ctx* c : g) {
     const int64_t lo = lo_of(c), hi = hi_of(c);
     for (int b = 0; b < addr.nblocks; ++b) {
@@ -126,11 +208,11 @@ int exchange(const Group& g, const PlaneAddr& addr, bool dir_up, bool dir_down, 
             UC_CUDA_OK(cudaMemcpyAsync(addr.glo(c->hi_local, b), addr.top(c, b),
                                        sizeof(double) * addr.count(c), cudaMemcpyDeviceToDevice, s));
           } else if (c->hi_rank >= 0) {
-            UC_NCCL_OK(g_nccl.send(addr.top(c, b), addr.count(c), kNcclFloat64, c->hi_rank, g_nccl.comm, s));
+            if ((rc = send(addr.top(c, b), addr.count(c), c->hi_rank))) return rc;
           }
         }
         if (!c->lo_local && c->lo_rank >= 0 && ok(lo - 1))
-          UC_NCCL_OK(g_nccl.recv(addr.glo(c, b), addr.count(c), kNcclFloat64, c->lo_rank, g_nccl.comm, s));
+          if ((rc = recv(addr.glo(c, b), addr.count(c), c->lo_rank))) return rc;
       }
       if (dir_down) {
         // my bottom owned plane (lo) -> the lower neighbour's upper ghost
@@ -139,14 +221,15 @@ int exchange(const Group& g, const PlaneAddr& addr, bool dir_up, bool dir_down, 
             UC_CUDA_OK(cudaMemcpyAsync(addr.ghi(c->lo_local, b), addr.bottom(c, b),
                                        sizeof(double) * addr.count(c), cudaMemcpyDeviceToDevice, s));
           } else if (c->lo_rank >= 0) {
-            UC_NCCL_OK(g_nccl.send(addr.bottom(c, b), addr.count(c), kNcclFloat64, c->lo_rank, g_nccl.comm, s));
+            if ((rc = send(addr.bottom(c, b), addr.count(c), c->lo_rank))) return rc;
           }
         }
         if (!c->hi_local && c->hi_rank >= 0 && ok(hi))
-          UC_NCCL_OK(g_nccl.recv(addr.ghi(c, b), addr.count(c), kNcclFloat64, c->hi_rank, g_nccl.comm, s));
+          if ((rc = recv(addr.ghi(c, b), addr.count(c), c->hi_rank))) return rc;
       }
     }
   }
+  if (host) return host_flush(pend, s);
   if (remote) UC_NCCL_OK(g_nccl.groupEnd());
   return UC_OK;
 }
@@ -192,8 +275,19 @@ int global_sum(const Group& g, double* const* slots, bool do_sqrt, cudaStream_t 
     UC_CUDA_OK(cudaGetLastError());
   }
   if (remote) {
-    if (!g_nccl.comm) return set_error(UC_ERR_ARG, "remote neighbours but no NCCL communicator");
-    UC_NCCL_OK(g_nccl.allReduce(slots[0], slots[0], 1, kNcclFloat64, kNcclSum, g_nccl.comm, s));
+    if (g_host.active) {
+      int rc = host_stage(1);
+      if (rc) return rc;
+      UC_CUDA_OK(cudaMemcpyAsync(g_host.stage, slots[0], sizeof(double), cudaMemcpyDeviceToHost, s));
+      UC_CUDA_OK(cudaStreamSynchronize(s));
+      if (g_host.t.allreduce_sum(g_host.t.user, g_host.stage, 1) != 0)
+        return set_error(UC_ERR_CUDA, "host transport: allreduce callback failed");
+      UC_CUDA_OK(cudaMemcpyAsync(slots[0], g_host.stage, sizeof(double), cudaMemcpyHostToDevice, s));
+      UC_CUDA_OK(cudaStreamSynchronize(s));
+    } else {
+      if (!g_nccl.comm) return set_error(UC_ERR_ARG, "remote neighbours but no NCCL communicator");
+      UC_NCCL_OK(g_nccl.allReduce(slots[0], slots[0], 1, kNcclFloat64, kNcclSum, g_nccl.comm, s));
+    }
     SlotPtrs b{};
     for (int i = 0; i < n; ++i) b.p[i] = slots[i];
     b.p[0] = slots[0];
@@ -238,10 +332,27 @@ int uc_comm_init_nccl(const char* nccl_path, const void* id128, int rank, int nr
   return UC_OK;
 }
 
+int uc_comm_init_host(const uc_host_transport* t, int rank, int nranks) {
+  if (!t || !t->sendrecv || !t->allreduce_sum || rank < 0 || rank >= nranks)
+    return set_error(UC_ERR_ARG, "uc_comm_init_host: bad argument");
+  if (g_nccl.comm || g_host.active) return set_error(UC_ERR_ARG, "a communicator is already initialised");
+  g_host.t = *t;
+  g_host.rank = rank;
+  g_host.nranks = nranks;
+  g_host.active = true;
+  return UC_OK;
+}
+
 int uc_comm_finalize(void) {
   if (g_nccl.comm) {
     g_nccl.commDestroy(g_nccl.comm);
     g_nccl.comm = nullptr;
+  }
+  if (g_host.active) {
+    g_host.active = false;
+    if (g_host.stage) cudaFreeHost(g_host.stage);
+    g_host.stage = nullptr;
+    g_host.stage_n = 0;
   }
   return UC_OK;
 }
@@ -252,7 +363,7 @@ int uc_ctx_set_neighbors(uc_ctx* c, int lo_rank, int hi_rank) {
     return set_error(UC_ERR_ARG, "neighbour ranks do not match the slab boundaries");
   c->lo_rank = lo_rank;
   c->hi_rank = hi_rank;
-  c->dist = g_nccl.comm != nullptr && g_nccl.nranks > 1;
+  c->dist = (g_nccl.comm != nullptr && g_nccl.nranks > 1) || (g_host.active && g_host.nranks > 1);
   return UC_OK;
 }
 

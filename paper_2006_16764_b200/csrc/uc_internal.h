@@ -45,8 +45,9 @@ struct uc_ctx {
   // reduction workspace
   double* partials = nullptr;    // [UC_RED_GRID_MAX]
   unsigned int* ticket = nullptr;
-  double* scal = nullptr;        // [UC_SCAL_SLOTS] device scalars
-  double* pinned = nullptr;      // [UC_SCAL_SLOTS] pinned host staging
+  double* scal = nullptr;        // [scal_cap] device scalars (grown on demand by the Arnoldi step)
+  double* pinned = nullptr;      // [scal_cap] pinned host staging
+  int scal_cap = UC_SCAL_SLOTS;
   unsigned int* flags = nullptr;      // [4] sticky status flags (device alias)
   unsigned int* flags_host = nullptr; // mapped pinned host memory
   unsigned long long* locate_key = nullptr;
@@ -80,6 +81,7 @@ struct PlaneAddr {
 };
 // comm.cu
 bool group_has_remote(const Group& g);
+bool comm_is_host();  // remote neighbours go through the host-staged transport
 int exchange(const Group& g, const PlaneAddr& addr, bool dir_up, bool dir_down, cudaStream_t s);
 int global_sum(const Group& g, double* const* slots, bool do_sqrt, cudaStream_t s);
 bool group_needs_sum(const Group& g);
@@ -91,6 +93,8 @@ int reduce_dot(uc_ctx* c, int64_t n, const double* a, const double* b, double* o
 int nonfinite_flag(uc_ctx* c, int64_t n, const double* a, unsigned int* flag);
 int nonfinite_flag_on(cudaStream_t s, int64_t n, const double* a, unsigned int* flag);
 int launch_axpy(uc_ctx* c, int64_t n, const double* a, double s, const double* b, double* out);
+// grow the scalar workspace to at least `need` slots (synchronises the stream when it grows)
+int ensure_scal(uc_ctx* c, int64_t need);
 // residual.cu
 enum { MODE_NEW = 0, MODE_OLD = 1, MODE_JV = 2 };
 int launch_residual(uc_ctx* c, const uc_scheme* sc, int mode, const double* u,

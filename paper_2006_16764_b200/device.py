@@ -181,12 +181,21 @@ def combine(basis, k: int, y: np.ndarray) -> torch.Tensor:
     return out
 
 
+def _vec_check(x: torch.Tensor):
+    ctx = blas()
+    bad, nz = C.c_int32(), C.c_int32()
+    L.check(ctx.lib.uc_vec_check(ctx.bind(), x.numel(), L.ptr(x), C.byref(bad), C.byref(nz)), "uc_vec_check")
+    return bool(bad.value), bool(nz.value)
+
+
 def all_finite(x: torch.Tensor) -> bool:
-    return bool(torch.isfinite(x).all().item()) if x.numel() else True
+    """np.all(np.isfinite(x)) (newton.py:144,175) through k_vec_check."""
+    return not _vec_check(x)[0]
 
 
 def any_nonzero(x: torch.Tensor) -> bool:
-    return bool(torch.any(x != 0).item())
+    """np.any(x) (newton.py:176) through k_vec_check."""
+    return _vec_check(x)[1]
 
 
 def arnoldi(apply_op, basis: list, k: int, scale: float):

@@ -10,9 +10,58 @@ callers and tests that inspect them on small meshes.
 
 from __future__ import annotations
 
+from dataclasses import dataclass
+
 import numpy as np
 
-__all__ = ["StructuredMesh", "build_mesh", "gauss_rule", "mesh_descriptor"]
+__all__ = ["StructuredMesh", "QuadratureRule", "BasisEval", "build_mesh", "gauss_rule", "eval_basis",
+           "mesh_descriptor"]
+
+
+@dataclass(frozen=True)
+class QuadratureRule:
+    """Tensor Gauss rule on [-1, 1]^dim (mesh.py:26-36); also unpacks as
+    (points, weights)."""
+
+    points: np.ndarray   # (nq, dim)
+    weights: np.ndarray  # (nq,)
+
+    @property
+    def n_points(self) -> int:
+        return self.weights.size
+
+    def __iter__(self):
+        return iter((self.points, self.weights))
+
+    def __getitem__(self, i):
+        return (self.points, self.weights)[i]
+
+    def __len__(self):
+        return 2
+
+
+@dataclass
+class BasisEval:
+    """Shape functions at the quadrature points of one (every) element
+    (mesh.py:39-50): physical gradients, jxw = weight x Jacobian."""
+
+    values: np.ndarray     # (nq, nloc)
+    gradients: np.ndarray  # (nq, nloc, dim)
+    jxw: np.ndarray        # (nq,)
+
+
+def _lagrange_1d(order: int, x):
+    """1D Lagrange basis on [-1, 1] (mesh.py:63-79), same arithmetic."""
+    x = np.asarray(x, dtype=float)
+    if order == 1:
+        vals = np.stack([(1.0 - x) / 2.0, (1.0 + x) / 2.0], axis=-1)
+        ders = np.stack([-0.5 * np.ones_like(x), 0.5 * np.ones_like(x)], axis=-1)
+    elif order == 2:
+        vals = np.stack([x * (x - 1.0) / 2.0, 1.0 - x * x, x * (x + 1.0) / 2.0], axis=-1)
+        ders = np.stack([x - 0.5, -2.0 * x, x + 0.5], axis=-1)
+    else:
+        raise ValueError(f"unsupported element order {order}")
+    return vals, ders
 
 
 class StructuredMesh:
@@ -77,8 +126,60 @@ class StructuredMesh:
         cid = sum((idx[a] % 2) << a for a in range(self.dim))
         return [np.nonzero(cid == c)[0] for c in range(2 ** self.dim) if np.any(cid == c)]
 
+    # -- basis tables (constants of the mesh; mesh.py:104-176) -------------
+    def quadrature(self, points_per_axis: int = 3) -> QuadratureRule:
+        key = ("rule", points_per_axis)
+        if key not in self._lazy:
+            self._lazy[key] = gauss_rule(self.dim, points_per_axis)
+        return self._lazy[key]
+
+    def basis(self, rule=None) -> BasisEval:
+        rule = _as_rule(rule) if rule is not None else self.quadrature()
+        key = ("basis", rule.points.tobytes(), rule.weights.tobytes())
+        if key not in self._lazy:
+            self._lazy[key] = _tabulate_basis(self, rule)
+        return self._lazy[key]
+
     def __repr__(self):
         return f"StructuredMesh(dim={self.dim}, extents={self.extents}, counts={self.counts})"
+
+
+def _as_rule(rule) -> QuadratureRule:
+    if isinstance(rule, QuadratureRule):
+        return rule
+    pts, wts = (rule.points, rule.weights) if hasattr(rule, "points") else rule
+    return QuadratureRule(np.asarray(pts, dtype=float), np.asarray(wts, dtype=float))
+
+
+def _tabulate_basis(mesh, rule: QuadratureRule) -> BasisEval:
+    """Tensor Lagrange tables at the rule's points (mesh.py:151-176)."""
+    n1 = mesh.order + 1
+    vals1, ders1 = zip(*[_lagrange_1d(mesh.order, rule.points[:, a]) for a in range(mesh.dim)])
+    nq = rule.n_points
+    nloc = n1 ** mesh.dim
+    values = np.ones((nq, nloc))
+    gradients = np.zeros((nq, nloc, mesh.dim))
+    for loc in range(nloc):
+        idx = [(loc // n1 ** a) % n1 for a in range(mesh.dim)]
+        v = np.ones(nq)
+        for a in range(mesh.dim):
+            v = v * vals1[a][:, idx[a]]
+        values[:, loc] = v
+        for a in range(mesh.dim):
+            g = np.ones(nq)
+            for b in range(mesh.dim):
+                g = g * (ders1[b] if b == a else vals1[b])[:, idx[b]]
+            gradients[:, loc, a] = g * (2.0 / mesh.spacing[a])
+    detj = np.prod([h / 2.0 for h in mesh.spacing])
+    return BasisEval(values=values, gradients=gradients, jxw=rule.weights * detj)
+
+
+def eval_basis(mesh, element_id: int, rule=None) -> BasisEval:
+    """Basis values/gradients/weights of one element, identical for all
+    (mesh.py:259-265)."""
+    if not 0 <= element_id < mesh.n_elements:
+        raise IndexError(f"element id {element_id} out of range")
+    return mesh.basis(rule)
 
 
 def build_mesh(dim: int, extents, counts, order: int = 1) -> StructuredMesh:
@@ -100,14 +201,14 @@ def build_mesh(dim: int, extents, counts, order: int = 1) -> StructuredMesh:
     return StructuredMesh(dim, extents, counts, order)
 
 
-def gauss_rule(dim: int, points_per_axis: int = 3):
-    """(points, weights) of the tensor Gauss rule, x fastest (mesh.py:52-61)."""
+def gauss_rule(dim: int, points_per_axis: int = 3) -> QuadratureRule:
+    """Tensor Gauss rule, x fastest (mesh.py:52-61); unpacks as (points, weights)."""
     x, w = np.polynomial.legendre.leggauss(points_per_axis)
     pts = np.stack([g.reshape(-1) for g in np.meshgrid(*([x] * dim), indexing="ij")[::-1]], axis=1)
     wts = np.ones(points_per_axis ** dim)
     for g in np.meshgrid(*([w] * dim), indexing="ij"):
         wts = wts * g.reshape(-1)
-    return pts, wts
+    return QuadratureRule(points=pts, weights=wts)
 
 
 def mesh_descriptor(mesh, slab=None):

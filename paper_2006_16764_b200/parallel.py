@@ -26,6 +26,7 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
 
 import numpy as np
 import torch
@@ -164,8 +165,9 @@ class SlabSpace:
 class SlabGroup:
     """The slabs of one mesh/model driven by this process."""
 
-    def __init__(self, mesh, kernel, slabs, dist_rank=None, dist_world=None):
-        self._args = (mesh, kernel, list(slabs), dist_rank, dist_world)
+    def __init__(self, mesh, kernel, slabs, dist_rank=None, dist_world=None, pg=None):
+        self._args = (mesh, kernel, list(slabs), dist_rank, dist_world, pg)
+        self._pg = pg  # torch.distributed process group of the ranks (None = WORLD)
         self.mesh = mesh
         self.kernel = kernel
         self.slabs = list(slabs)
@@ -190,24 +192,31 @@ class SlabGroup:
         return cls(mesh, kernel, slab_bounds(mesh, world, levels))
 
     @classmethod
-    def from_torch_dist(cls, mesh, kernel, levels: int = 4, group=None):
+    def from_torch_dist(cls, mesh, kernel, levels: int = 4, group=None, transport: str = "nccl"):
         """One slab per torch.distributed rank; initialises the library's NCCL
-        communicator from a unique id broadcast over torch.distributed."""
+        communicator from a unique id broadcast over torch.distributed.
+        transport="host": the same remote code path with planes and partial
+        sums staged through host memory and moved by torch.distributed (gloo);
+        for several ranks sharing one GPU, where NCCL cannot run (tests)."""
         import torch.distributed as dist
 
         rank, world = dist.get_rank(group), dist.get_world_size(group)
         path = nccl_library_path()
         lib = L.load()
-        if world > 1:
+        if world > 1 and transport == "host":
+            HostTransportCallbacks.install(group, rank, world)
+        elif world > 1:
             idb = (C.c_char * 128)()
             if rank == 0:
                 L.check(lib.uc_nccl_unique_id(path.encode(), idb), "uc_nccl_unique_id")
             obj = [bytes(idb)]
-            dist.broadcast_object_list(obj, src=0, group=group)
+            src = 0 if group is None else dist.get_global_rank(group, 0)
+            dist.broadcast_object_list(obj, src=src, group=group)
             idb = (C.c_char * 128).from_buffer_copy(obj[0])
             L.check(lib.uc_comm_init_nccl(path.encode(), idb, rank, world), "uc_comm_init_nccl")
         bounds = slab_bounds(mesh, world, levels)
-        return cls(mesh, kernel, [bounds[rank]], dist_rank=rank if world > 1 else None, dist_world=world)
+        return cls(mesh, kernel, [bounds[rank]], dist_rank=rank if world > 1 else None, dist_world=world,
+                   pg=group)
 
     def clone(self) -> "SlabGroup":
         """Fresh contexts on the same slabs (a preconditioner owns its own)."""
@@ -242,10 +251,65 @@ class SlabGroup:
         if self._dist:
             import torch.distributed as dist
 
-            t = torch.tensor([1.0 if bad else 0.0], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dev = "cpu" if dist.get_backend(self._pg) == "gloo" else "cuda"
+            t = torch.tensor([1.0 if bad else 0.0], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX, group=self._pg)
             bad = bool(t.item() > 0)
         return bad
+
+
+class HostTransportCallbacks:
+    """uc_comm_init_host callbacks over torch.distributed (CPU tensors aliasing
+    the library's pinned staging buffers; every call completes before it
+    returns)."""
+
+    _live = None  # keeps the ctypes callbacks alive while the library holds them
+
+    def __init__(self, group):
+        self.group = group
+        self._sr = L.SENDRECV_FN(self._sendrecv)
+        self._ar = L.ALLREDUCE_FN(self._allreduce)
+        self.struct = L.HostTransport(None, self._sr, self._ar)
+
+    @classmethod
+    def install(cls, group, rank, world):
+        cb = cls(group)
+        L.check(L.load().uc_comm_init_host(C.byref(cb.struct), rank, world), "uc_comm_init_host")
+        cls._live = cb
+        return cb
+
+    def _peer(self, r):
+        import torch.distributed as dist
+
+        return r if self.group is None else dist.get_global_rank(self.group, r)
+
+    def _sendrecv(self, user, nops, ops):
+        import torch.distributed as dist
+
+        try:
+            reqs = []
+            for i in range(nops):
+                op = ops[i]
+                t = torch.from_numpy(np.ctypeslib.as_array(op.buf, shape=(op.count,)))
+                fn = dist.isend if op.kind == 0 else dist.irecv
+                reqs.append(fn(t, self._peer(op.peer), group=self.group))
+            for r in reqs:
+                r.wait()
+            return 0
+        except Exception as exc:  # reported through the library's error path
+            print(f"host transport sendrecv failed: {exc!r}", file=sys.stderr)
+            return 1
+
+    def _allreduce(self, user, vals, n):
+        import torch.distributed as dist
+
+        try:
+            t = torch.from_numpy(np.ctypeslib.as_array(vals, shape=(n,)))
+            dist.all_reduce(t, group=self.group)
+            return 0
+        except Exception as exc:
+            print(f"host transport allreduce failed: {exc!r}", file=sys.stderr)
+            return 1
 
 
 def nccl_library_path() -> str:

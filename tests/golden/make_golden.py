@@ -485,8 +485,85 @@ def subset_cases(meta):
         print("subset", name)
 
 
+DROPIN_CASES = [
+    # name, model, dim, extents, counts
+    ("fg2d", "free_growth", 2, (0.48, 0.36), (16, 12)),
+    ("al3d", "alloy", 3, (4.8, 3.2, 2.4), (6, 4, 3)),
+]
+
+
+def dropin_cases(meta):
+    """frozen_quad_state (assembly.py:193-211), eval_basis (mesh.py:259-265) and
+    assemble_field_matrix (assembly.py:271-303) with per-point, scalar and
+    non-default-rule coefficients."""
+    for name, model, dim, ext, cnt in DROPIN_CASES:
+        mesh = uc.build_mesh(dim, ext, cnt)
+        k = kernel_for(model)
+        n, ne = mesh.n_nodes, mesh.n_elements
+        rng = np.random.default_rng(21)
+        state = fg_state(rng, n) if model == "free_growth" else alloy_state(rng, n)
+        scheme = uc.ThetaScheme(0.5, 3e-4, 2)
+        qs = uc.assembly.frozen_quad_state(mesh, k, state, scheme)
+        out = dict(state=state, coords=qs.coords)
+        for f in range(k.n_fields):
+            out[f"val{f}"] = qs.val_new[f]
+            for d in range(dim):
+                out[f"grad{f}_{d}"] = qs.grad_new[f][d]
+        for ppa in (2, 3, 4):
+            rule = uc.gauss_rule(dim, ppa)
+            b = uc.eval_basis(mesh, 0, rule)
+            out[f"basis{ppa}_values"] = b.values
+            out[f"basis{ppa}_gradients"] = b.gradients
+            out[f"basis{ppa}_jxw"] = b.jxw
+        nq = 3 ** dim
+        cm = 0.5 + rng.random((ne, nq))
+        cd = 0.1 + rng.random((ne, nq))
+        out.update(cm=cm, cd=cd)
+        for tag, a, b_, rule in (("qp", cm, cd, None), ("scalar", 2.5, 0.75, None),
+                                  ("rule2", cm[:, : 2 ** dim] * 1.0, 0.75, uc.gauss_rule(dim, 2))):
+            mat = uc.assemble_field_matrix(mesh, a, b_, rule).tocsr()
+            mat.sort_indices()
+            out[f"M{tag}_data"] = mat.data
+            out[f"M{tag}_indices"] = mat.indices
+            out[f"M{tag}_indptr"] = mat.indptr
+        np.savez_compressed(os.path.join(OUT, f"dropin_{name}.npz"), **out)
+        meta[f"dropin_{name}"] = dict(model=model, dim=dim, extents=ext, counts=cnt, theta=0.5, dt=3e-4, step=2)
+
+
+def survey_case(meta):
+    """configs[1] at full size: two implicit steps of the seeded dendrite at
+    2048^2 through the reference's own simulate() (default solver; ~8 min)."""
+    cfg = default_config("free_growth")
+    cfg.mesh.extents, cfg.mesh.counts = (61.44, 61.44), (2048, 2048)
+    cfg.time.t_final = 2 * cfg.time.dt
+    cfg.precond.ordering = "multicolor"
+    t0 = time.perf_counter()
+    res = simulate(cfg)
+    recs = res.records
+    meta["survey_fg2d_2048_2"] = dict(
+        model="free_growth", dim=2, extents=(61.44, 61.44), counts=(2048, 2048), dt=cfg.time.dt, steps=2,
+        status=res.status, newton=[r["newton_iters"] for r in recs], gmres=[r["gmres_iters"] for r in recs],
+        fnorm=[float(r["fnorm"]) for r in recs], fnorm0=[float(r["fnorm0"]) for r in recs],
+        theta=cfg.time.theta, startup_steps=cfg.time.startup_steps, wall_seconds=time.perf_counter() - t0,
+        source="reference simulate() via tests/golden/make_golden.py --only-survey")
+    print("survey", meta["survey_fg2d_2048_2"], flush=True)
+
+
 def main():
     meta = {"generator": "tests/golden/make_golden.py", "reference": REF}
+    if "--only-survey" in sys.argv:
+        survey_case(meta)
+        full = json.load(open(os.path.join(OUT, "golden.json")))
+        full.update({k: v for k, v in meta.items() if k.startswith("survey_")})
+        with open(os.path.join(OUT, "golden.json"), "w") as fh:
+            json.dump(full, fh, indent=1, sort_keys=True)
+        return
+    if "--only-dropin" in sys.argv:
+        meta = json.load(open(os.path.join(OUT, "golden.json")))
+        dropin_cases(meta)
+        with open(os.path.join(OUT, "golden.json"), "w") as fh:
+            json.dump(meta, fh, indent=1, sort_keys=True)
+        return
     if "--only-massdiff" in sys.argv:
         meta = json.load(open(os.path.join(OUT, "golden.json")))
         massdiff_cases(meta)
@@ -515,6 +592,7 @@ def main():
         precond_cases(meta)
         newton_case(meta)
         ic_cases(meta)
+        dropin_cases(meta)
     old = json.load(open(os.path.join(OUT, "golden.json"))) if os.path.exists(os.path.join(OUT, "golden.json")) else {}
     if "--only-runs" in sys.argv:
         meta = old
@@ -526,11 +604,7 @@ def main():
         writer_cases(meta)
     else:
         meta.update({k: v for k, v in old.items() if k.startswith("run_")})
-    # measured with the reference in SURVEY.md section 8(c) (453 s on this host):
-    # free growth 2048^2, 2 steps, default solver, multicolor == lexicographic counts
-    meta["survey_fg2d_2048_2"] = dict(model="free_growth", dim=2, extents=(61.44, 61.44),
-                                      counts=(2048, 2048), dt=2.25e-4, steps=2, newton=[4, 3],
-                                      gmres=[16, 12], source="SURVEY.md 8(c) / BASELINE.md 4.1")
+    meta.update({k: v for k, v in old.items() if k.startswith("survey_") and k not in meta})
     with open(os.path.join(OUT, "golden.json"), "w") as fh:
         json.dump(meta, fh, indent=1, sort_keys=True)
 
