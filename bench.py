@@ -183,6 +183,7 @@ def run_reference(args, w, rank, world):
     rows = None if w["dim"] == 2 and np.prod(w["counts"]) <= 2048 * 2048 else 256
     sec, D, sample, cores = cpu_oracle_step_time(w, steps=args.steps, warmup=args.warmup, rows=rows)
     mdofs = 2 * D / sec / 1e6
+    ref_py = reference_python_1core(args.workload) if not args.no_cpu_baseline else None
     line = {
         "impl": "reference", "metric": "MDoF/s residual+Jv fill", "value": round(mdofs, 4),
         "unit": "MDoF/s", "n_gpus": args.gpus, "device": "host cores only", "steps": args.steps,
@@ -191,11 +192,32 @@ def run_reference(args, w, rank, world):
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": args.workload, **{k: w[k] for k in ("model", "dim", "counts")}},
         "cpu_baseline": {"value": round(mdofs, 4), "unit": "MDoF/s", "cores": cores, "kind": "port",
-                         "sample": sample},
+                         "sample": sample + f"; {cores}-thread OpenMP C port of the reference (oracle/uc_oracle.c)"},
         "e2e": {"value": round(mdofs, 4), "unit": "MDoF/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
+        "reference_python_1core": ref_py,
     }
     print(json.dumps(line), flush=True)
+
+
+def reference_python_1core(workload):
+    """The reference package itself (undercool, baseline/_ref) on one pinned
+    core, beside the C port; None if not installed."""
+    if not os.path.isdir(os.path.join(ROOT, "baseline", "_ref", "undercool")):
+        return None
+    env = dict(os.environ, OPENBLAS_NUM_THREADS="1", OMP_NUM_THREADS="1", MKL_NUM_THREADS="1",
+               NUMBA_NUM_THREADS="1")
+    cmd = [sys.executable, os.path.join(ROOT, "tools", "ref_python_time.py"), workload, "10"]
+    try:
+        cmd = ["taskset", "-c", str(sorted(os.sched_getaffinity(0))[0])] + cmd
+    except (AttributeError, OSError):
+        pass
+    try:
+        r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
+        lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+        return json.loads(lines[-1]) if lines else {"value": None, "error": r.stderr[-300:]}
+    except Exception as exc:  # reported, never fatal
+        return {"value": None, "error": repr(exc)}
 
 
 def vcycle_bytes(pc, N, dim):
@@ -376,7 +398,10 @@ def run_slabs(args, w, rank, world, local, dist, emulate=0):
             r0 = SlabResidual(grp, st, st, sc0)
             barrier()
             t0 = time.perf_counter()
-            _, rep = uc.newton_solve(r0, st, uc.NewtonConfig(), precond_apply=pc.apply)
+            # CGS2 Arnoldi: two vector allreduces per step instead of 2(k+1)
+            # scalar ones (same counts as MGS: tests/test_gpu_cgs2.py)
+            _, rep = uc.newton_solve(r0, st, uc.NewtonConfig(gmres=uc.GmresConfig(orthogonalization="cgs2")),
+                                     precond_apply=pc.apply)
             barrier()
             walls.append(max_ms(time.perf_counter() - t0))
         t_newton = float(np.median(walls[1:]))
@@ -387,7 +412,8 @@ def run_slabs(args, w, rank, world, local, dist, emulate=0):
                   "converged": bool(rep.converged), "precond_build_s": round(t_build, 4),
                   "cold_sec_per_newton_iteration": round(walls[0] / max(rep.iterations, 1), 5),
                   "vcycle_apply_ms": round(t_apply, 3),
-                  "case": "seed IC, step 0 (backward-Euler startup), default solver settings, slabs",
+                  "case": "seed IC, step 0 (backward-Euler startup), default solver settings except "
+                          "CGS2 Arnoldi, slabs",
                   "ordering": "multicolor", "timing": "host wall clock per solve, max over ranks"}
         pc = r0 = None
 
@@ -428,6 +454,13 @@ def roofline_kernel_name(w):
     return f"k_residual<{w['dim']},{'FG' if w['model'] == 'free_growth' else 'ALLOY'},NEW>"
 
 
+def reference_python_1core_for(w):
+    for name, ww in WORKLOADS.items():
+        if ww is w or ww == w:
+            return reference_python_1core(name)
+    return None
+
+
 def cpu_baseline_line(w):
     """The CPU port of the reference on this host's cores, bounded sample."""
     N = int(np.prod([c + 1 for c in w["counts"]]))
@@ -437,7 +470,9 @@ def cpu_baseline_line(w):
                                                      min_seconds=10.0)
         return {"value": round(2 * Dc / sec / 1e6, 4), "unit": "MDoF/s", "cores": cores,
                 "kind": "port", "sample": sample + "; residual+Jv of oracle/uc_oracle.c (OpenMP, "
-                                                   f"{cores}-thread C port of the reference)"}
+                                                   f"{cores}-thread C port of the reference)",
+                "label": f"{cores}-thread C port",
+                "reference_python_1core": reference_python_1core_for(w)}
     except Exception as exc:  # reported, not fatal
         return {"value": None, "unit": "MDoF/s", "cores": 0, "kind": "port", "sample": f"failed: {exc}"}
 

@@ -192,6 +192,16 @@ int uc_norm_host(uc_ctx* ctx, int64_t n, const double* a, double* out);
 int uc_arnoldi(uc_ctx* ctx, int64_t n, const double* const* basis, int k,
                double* w, double scale, double* h_host, int* broke);
 
+/* arnoldi_step with classical Gram-Schmidt applied twice (CGS2): the same
+ * projections as uc_arnoldi's MGS + re-orthogonalisation (krylov.py:48-70)
+ * computed pass-wise, so a distributed step needs two (k+1)-value global sums
+ * and one norm instead of 2(k+1) scalar sums.  Opt-in
+ * (GmresConfig.orthogonalization = "cgs2"); k + 1 <= 256. */
+int uc_arnoldi_cgs2(uc_ctx* ctx, int64_t n, const double* const* basis, int k, double* w,
+                    double scale, double* h_host, int* broke);
+int uc_arnoldi_cgs2_group(uc_ctx* const* ctxs, int nslabs, const double* const* basis, int k,
+                          double* const* w, double scale, double* h_host, int* broke);
+
 /* out = sum_j y[j] * basis[j], j = 0..k-1 (krylov.py:180-182 basis[:k].T @ y). */
 int uc_combine(uc_ctx* ctx, int64_t n, const double* const* basis, int k,
                const double* y_host, double* out);

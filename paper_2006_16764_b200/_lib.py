@@ -93,6 +93,9 @@ SIGNATURES = {
     "uc_norm_host": (_I, [_P, _I64, _P, C.POINTER(_D)]),
     "uc_arnoldi": (_I, [_P, _I64, C.POINTER(_P), _I, _P, _D, C.POINTER(_D), C.POINTER(_I)]),
     "uc_combine": (_I, [_P, _I64, C.POINTER(_P), _I, C.POINTER(_D), _P]),
+    "uc_arnoldi_cgs2": (_I, [_P, _I64, C.POINTER(_P), _I, _P, _D, C.POINTER(_D), C.POINTER(_I)]),
+    "uc_arnoldi_cgs2_group": (_I, [C.POINTER(_P), _I, C.POINTER(_P), _I, C.POINTER(_P), _D,
+                                   C.POINTER(_D), C.POINTER(_I)]),
     "uc_axpy": (_I, [_P, _I64, _P, _D, _P, _P]),
     "uc_sub": (_I, [_P, _I64, _P, _P, _P]),
     "uc_scale_div": (_I, [_P, _I64, _P, _D, _P]),

@@ -334,6 +334,135 @@ static int arnoldi_group(const Group& G, const int64_t* n, const double* const* 
   return UC_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Classical Gram-Schmidt with one re-orthogonalisation (CGS2): h = V^T w,
+// w -= V h, twice, then |w|.  Mathematically the MGS + reorthogonalisation of
+// krylov.py:48-70; the projections of a pass are computed together, so a
+// distributed step needs three global sums (two of k+1 values and the norm)
+// instead of 2(k+1) scalar ones.  Opt-in (GmresConfig.orthogonalization).
+// ---------------------------------------------------------------------------
+#define UC_MDOT_B 8
+struct MdotArgs {
+  const double* v[UC_MDOT_B];
+  int nb;
+};
+// partial dots of w with up to 8 basis vectors; the last CTA sums the per-CTA
+// partials in index order (deterministic)
+__global__ void __launch_bounds__(UC_RED_THREADS) k_mdot(int64_t n, const MdotArgs a, const double* __restrict__ w,
+                                                         double* partials, unsigned int* ticket, double* out) {
+  __shared__ double sh[UC_MDOT_B][UC_RED_THREADS / 32];
+  __shared__ bool last;
+  double acc[UC_MDOT_B];
+#pragma unroll
+  for (int j = 0; j < UC_MDOT_B; ++j) acc[j] = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double wi = w[i];
+#pragma unroll
+    for (int j = 0; j < UC_MDOT_B; ++j)
+      if (j < a.nb) acc[j] += __ldg(a.v[j] + i) * wi;
+  }
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j < UC_MDOT_B; ++j) {
+    double v = acc[j];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) sh[j][wid] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < a.nb) {
+    double s = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) s += sh[threadIdx.x][q];
+    partials[threadIdx.x * gridDim.x + blockIdx.x] = s;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (threadIdx.x < a.nb) {
+    double s = 0.0;
+    for (unsigned b = 0; b < gridDim.x; ++b) s += __ldcg(partials + threadIdx.x * gridDim.x + b);
+    out[threadIdx.x] = s;
+  }
+  if (threadIdx.x == 0) *ticket = 0u;
+}
+
+#define UC_CGS_MAXV 256
+struct MupdArgs {
+  const double* v[UC_CGS_MAXV];
+  int m;
+};
+// w -= sum_j h[j] V_j (j in order); with acc != NULL also h_acc[j] += h[j]
+__global__ void k_cgs_update(int64_t n, const __grid_constant__ MupdArgs a, const double* __restrict__ h,
+                             double* __restrict__ w, double* h_acc) {
+  if (h_acc && blockIdx.x == 0)
+    for (int j = threadIdx.x; j < a.m; j += blockDim.x) h_acc[j] += h[j];
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+    double s = 0.0;
+    for (int j = 0; j < a.m; ++j) s += __ldg(h + j) * __ldg(a.v[j] + i);
+    w[i] = __dsub_rn(w[i], s);
+  }
+}
+
+static int cgs2_group(const Group& G, const int64_t* n, const double* const* const* basis, int k, double* const* w,
+                      double scale, double* h_host, int* broke) {
+  const int ns = (int)G.size();
+  if (k < 0 || k + 1 > UC_CGS_MAXV) return set_error(UC_ERR_ARG, "cgs2: k=%d out of range", k);
+  for (uc_ctx* c : G)
+    if (int rc0 = ensure_scal(c, 3 * (int64_t)(k + 2) + 8)) return rc0;
+  cudaStream_t s = G[0]->stream;
+  const bool sum = group_needs_sum(G);
+  const int m = k + 1;
+  int rc;
+  // per slab scalar layout: h [0, k+2); pass-2 projections [k+2, 2k+4)
+  for (int pass = 0; pass < 2; ++pass) {
+    std::vector<double*> slot(ns);
+    for (int i = 0; i < ns; ++i) {
+      uc_ctx* c = G[i];
+      double* hp = c->scal + (pass == 0 ? 0 : (k + 2));
+      slot[i] = hp;
+      for (int j0 = 0; j0 < m; j0 += UC_MDOT_B) {
+        MdotArgs a{};
+        a.nb = m - j0 < UC_MDOT_B ? m - j0 : UC_MDOT_B;
+        for (int j = 0; j < a.nb; ++j) a.v[j] = basis[i][j0 + j];
+        k_mdot<<<red_grid(n[i]), UC_RED_THREADS, 0, s>>>(n[i], a, w[i], c->partials, c->ticket, hp + j0);
+        UC_CUDA_OK(cudaGetLastError());
+      }
+    }
+    if (sum && (rc = global_sum_n(G, slot.data(), m, s))) return rc;
+    for (int i = 0; i < ns; ++i) {
+      uc_ctx* c = G[i];
+      static MupdArgs u;
+      u.m = m;
+      for (int j = 0; j < m; ++j) u.v[j] = basis[i][j];
+      k_cgs_update<<<ew_grid(c, n[i]), 256, 0, s>>>(n[i], u, slot[i], w[i], pass == 1 ? c->scal : nullptr);
+      UC_CUDA_OK(cudaGetLastError());
+    }
+  }
+  // h[k+1] = |w|
+  std::vector<double*> nrm(ns);
+  for (int i = 0; i < ns; ++i) {
+    nrm[i] = &G[i]->scal[k + 1];
+    if ((rc = reduce_dot(G[i], n[i], w[i], w[i], nrm[i], !sum))) return rc;
+  }
+  if (sum && (rc = global_sum(G, nrm.data(), true, s))) return rc;
+  const double tol = 1e-14 * scale;  // BREAKDOWN_TOL * scale (krylov.py:13,67)
+  for (int i = 0; i < ns; ++i) {
+    k_normalize<<<ew_grid(G[i], n[i]), 256, 0, s>>>(n[i], w[i], &G[i]->scal[k + 1], tol,
+                                                    const_cast<double*>(basis[i][k + 1]));
+    UC_CUDA_OK(cudaGetLastError());
+  }
+  UC_CUDA_OK(cudaMemcpyAsync(G[0]->pinned, G[0]->scal, sizeof(double) * (k + 2), cudaMemcpyDeviceToHost, s));
+  UC_CUDA_OK(cudaStreamSynchronize(s));
+  for (int i = 0; i < k + 2; ++i) h_host[i] = G[0]->pinned[i];
+  *broke = (h_host[k + 1] < tol) ? 1 : 0;
+  return UC_OK;
+}
+
 int uc_arnoldi(uc_ctx* c, int64_t n, const double* const* basis, int k, double* w, double scale,
                double* h_host, int* broke) {
   if (!c || !basis || !w) return set_error(UC_ERR_ARG, "uc_arnoldi: bad argument");
@@ -353,6 +482,26 @@ int uc_arnoldi_group(uc_ctx* const* ctxs, int nslabs, const double* const* basis
     b[i] = basis + (size_t)i * (k + 2);
   }
   return arnoldi_group(G, n.data(), b.data(), k, w, scale, h_host, broke);
+}
+
+int uc_arnoldi_cgs2_group(uc_ctx* const* ctxs, int nslabs, const double* const* basis, int k,
+                          double* const* w, double scale, double* h_host, int* broke) {
+  if (!ctxs || nslabs < 1 || !basis || !w) return set_error(UC_ERR_ARG, "uc_arnoldi_cgs2_group: bad argument");
+  Group G(ctxs, ctxs + nslabs);
+  std::vector<int64_t> n(nslabs);
+  std::vector<const double* const*> b(nslabs);
+  for (int i = 0; i < nslabs; ++i) {
+    n[i] = vec_len(G[i]);
+    b[i] = basis + (size_t)i * (k + 2);
+  }
+  return cgs2_group(G, n.data(), b.data(), k, w, scale, h_host, broke);
+}
+
+int uc_arnoldi_cgs2(uc_ctx* c, int64_t n, const double* const* basis, int k, double* w, double scale,
+                    double* h_host, int* broke) {
+  if (!c || !basis || !w) return set_error(UC_ERR_ARG, "uc_arnoldi_cgs2: bad argument");
+  Group G{c};
+  return cgs2_group(G, &n, &basis, k, &w, scale, h_host, broke);
 }
 
 int uc_combine(uc_ctx* c, int64_t n, const double* const* basis, int k, const double* y,

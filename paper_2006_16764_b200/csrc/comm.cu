@@ -303,6 +303,46 @@ int global_sum(const Group& g, double* const* slots, bool do_sqrt, cudaStream_t 
   return UC_OK;
 }
 
+__global__ void k_sum_slots_n(SlotPtrs a, int n) {
+  for (int j = threadIdx.x; j < n; j += blockDim.x) {
+    double s = 0.0;
+    for (int i = 0; i < a.n; ++i) s += a.p[i][j];
+    for (int i = 0; i < a.n; ++i) a.p[i][j] = s;
+  }
+}
+
+// slots[i] holds slab i's local partial sums (n values); afterwards every slot
+// holds the global sums (slabs in order, then ranks by allreduce).
+int global_sum_n(const Group& g, double* const* slots, int n, cudaStream_t s) {
+  const int ns = (int)g.size();
+  if (ns > 16) return set_error(UC_ERR_ARG, "at most 16 local slabs per group");
+  const bool remote = group_dist(g);
+  SlotPtrs a{};
+  for (int i = 0; i < ns; ++i) a.p[i] = slots[i];
+  a.n = ns;
+  if (ns > 1) {
+    k_sum_slots_n<<<1, 256, 0, s>>>(a, n);
+    UC_CUDA_OK(cudaGetLastError());
+  }
+  if (!remote) return UC_OK;
+  if (g_host.active) {
+    int rc = host_stage((size_t)n);
+    if (rc) return rc;
+    UC_CUDA_OK(cudaMemcpyAsync(g_host.stage, slots[0], sizeof(double) * n, cudaMemcpyDeviceToHost, s));
+    UC_CUDA_OK(cudaStreamSynchronize(s));
+    if (g_host.t.allreduce_sum(g_host.t.user, g_host.stage, n) != 0)
+      return set_error(UC_ERR_CUDA, "host transport: allreduce callback failed");
+    UC_CUDA_OK(cudaMemcpyAsync(slots[0], g_host.stage, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+    UC_CUDA_OK(cudaStreamSynchronize(s));
+  } else {
+    if (!g_nccl.comm) return set_error(UC_ERR_ARG, "remote neighbours but no NCCL communicator");
+    UC_NCCL_OK(g_nccl.allReduce(slots[0], slots[0], (size_t)n, kNcclFloat64, kNcclSum, g_nccl.comm, s));
+  }
+  for (int i = 1; i < ns; ++i)
+    UC_CUDA_OK(cudaMemcpyAsync(slots[i], slots[0], sizeof(double) * n, cudaMemcpyDeviceToDevice, s));
+  return UC_OK;
+}
+
 }  // namespace uc
 
 using namespace uc;

@@ -84,6 +84,7 @@ bool group_has_remote(const Group& g);
 bool comm_is_host();  // remote neighbours go through the host-staged transport
 int exchange(const Group& g, const PlaneAddr& addr, bool dir_up, bool dir_down, cudaStream_t s);
 int global_sum(const Group& g, double* const* slots, bool do_sqrt, cudaStream_t s);
+int global_sum_n(const Group& g, double* const* slots, int n, cudaStream_t s);
 bool group_needs_sum(const Group& g);
 // exchange ghost planes of unpadded block vectors vecs[i] into ghost slot `slot`
 int halo_vectors(const Group& g, int slot, const double* const* vecs, cudaStream_t s);

@@ -198,7 +198,7 @@ def any_nonzero(x: torch.Tensor) -> bool:
     return _vec_check(x)[1]
 
 
-def arnoldi(apply_op, basis: list, k: int, scale: float):
+def arnoldi(apply_op, basis: list, k: int, scale: float, cgs2: bool = False):
     """One Arnoldi step (krylov.py:48-70) on device vectors: (h numpy, new
     vector or None, breakdown)."""
     w = as_device(apply_op(basis[k]))
@@ -208,8 +208,9 @@ def arnoldi(apply_op, basis: list, k: int, scale: float):
     h = np.zeros(k + 2)
     broke = C.c_int()
     ctx = blas()
-    L.check(ctx.lib.uc_arnoldi(ctx.bind(), w.numel(), L.ptrs(basis[: k + 1] + [slot]), k, L.ptr(w),
-                               float(scale), h.ctypes.data_as(C.POINTER(C.c_double)), C.byref(broke)),
+    fn = ctx.lib.uc_arnoldi_cgs2 if cgs2 else ctx.lib.uc_arnoldi
+    L.check(fn(ctx.bind(), w.numel(), L.ptrs(basis[: k + 1] + [slot]), k, L.ptr(w),
+               float(scale), h.ctypes.data_as(C.POINTER(C.c_double)), C.byref(broke)),
             "uc_arnoldi")
     if broke.value:
         return h, None, True

@@ -140,7 +140,7 @@ class SlabSpace:
     def any_nonzero(self, x):
         return self.norm(x) != 0.0
 
-    def arnoldi(self, apply_op, basis, k, scale):
+    def arnoldi(self, apply_op, basis, k, scale, cgs2: bool = False):
         w = apply_op(basis[k])
         parts = []
         for i, p in enumerate(w.parts):
@@ -154,9 +154,9 @@ class SlabSpace:
             mat += [b.parts[i] for b in basis[: k + 1]] + [slot.parts[i]]
         h = np.zeros(k + 2)
         broke = C.c_int()
-        L.check(L.load().uc_arnoldi_group(self._ctxs(), ns, L.ptrs(mat), k, L.ptrs(parts), float(scale),
-                                          h.ctypes.data_as(C.POINTER(C.c_double)), C.byref(broke)),
-                "uc_arnoldi_group")
+        fn = L.load().uc_arnoldi_cgs2_group if cgs2 else L.load().uc_arnoldi_group
+        L.check(fn(self._ctxs(), ns, L.ptrs(mat), k, L.ptrs(parts), float(scale),
+                   h.ctypes.data_as(C.POINTER(C.c_double)), C.byref(broke)), "uc_arnoldi_group")
         if broke.value:
             return h, None, True
         return h, slot, False

@@ -15,7 +15,7 @@ import numpy as np
 import pytest
 import torch
 
-from conftest import golden, golden_meta, rel
+from conftest import golden_meta
 
 pytestmark = pytest.mark.gpu
 META = golden_meta()
@@ -31,7 +31,7 @@ def _free_port():
     return port
 
 
-def _run(grp, uc, models, k, mesh, m):
+def _run(grp, uc, models, k, mesh, m, ortho="mgs"):
     """residual, Jv, V-cycle application and STEPS implicit steps on a slab group;
     returns the slab parts of every result (this process's slabs)."""
     from paper_2006_16764_b200.parallel import SlabPrecond, SlabResidual
@@ -55,8 +55,8 @@ def _run(grp, uc, models, k, mesh, m):
         th = 1.0 if step < m["startup_steps"] else m["theta"]
         sc = uc.ThetaScheme(th, m["dt"], step)
         pc = SlabPrecond(grp, state, sc, uc.PrecondConfig(ordering="multicolor"))
-        u, rep = uc.newton_solve(SlabResidual(grp, state, prev, sc), state, uc.NewtonConfig(),
-                                 precond_apply=pc.apply)
+        cfg = uc.NewtonConfig(gmres=uc.GmresConfig(orthogonalization=ortho))
+        u, rep = uc.newton_solve(SlabResidual(grp, state, prev, sc), state, cfg, precond_apply=pc.apply)
         assert rep.converged
         counts.append((rep.iterations, rep.total_gmres))
         prev, state = state, u
@@ -80,15 +80,17 @@ def _worker(rank, world, port, tmp):
         mesh = uc.build_mesh(m["dim"], m["extents"], m["counts"])
         k = uc.AlloyKernel()
         grp = SlabGroup.from_torch_dist(mesh, k, transport="host")
-        parts, counts = _run(grp, uc, models, k, mesh, m)
-        np.savez(os.path.join(tmp, f"rank{rank}.npz"), counts=np.array(counts),
-                 **{key: val[0] for key, val in parts.items()})
+        for ortho in ("mgs", "cgs2"):
+            parts, counts = _run(grp, uc, models, k, mesh, m, ortho)
+            np.savez(os.path.join(tmp, f"rank{rank}_{ortho}.npz"), counts=np.array(counts),
+                     **{key: val[0] for key, val in parts.items()})
     finally:
         L.load().uc_comm_finalize()
         dist.destroy_process_group()
 
 
 def test_two_rank_host_transport_equals_emulated_slabs(tmp_path):
+    """MGS (the reference's) and CGS2 Arnoldi, both through the rank branches."""
     import torch.multiprocessing as mp
 
     import paper_2006_16764_b200 as uc
@@ -98,17 +100,17 @@ def test_two_rank_host_transport_equals_emulated_slabs(tmp_path):
     world = 2
     mp.start_processes(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, start_method="spawn",
                        join=True)
-    ranks = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(world)]
-
     m = META[CASE]
     mesh = uc.build_mesh(m["dim"], m["extents"], m["counts"])
     k = uc.AlloyKernel()
     grp = SlabGroup(mesh, k, slab_bounds(mesh, world, 4))
-    local, counts = _run(grp, uc, models, k, mesh, m)
-    for key, parts in local.items():
+    for ortho in ("mgs", "cgs2"):
+        ranks = [dict(np.load(tmp_path / f"rank{r}_{ortho}.npz")) for r in range(world)]
+        local, counts = _run(grp, uc, models, k, mesh, m, ortho)
+        for key, parts in local.items():
+            for r in range(world):
+                assert np.array_equal(ranks[r][key].view(np.int64), parts[r].view(np.int64)), (ortho, key, r)
         for r in range(world):
-            assert np.array_equal(ranks[r][key].view(np.int64), parts[r].view(np.int64)), (key, r)
-    for r in range(world):
-        assert [tuple(c) for c in ranks[r]["counts"]] == counts
-    assert [c[0] for c in counts] == m["newton"][:STEPS]
-    assert [c[1] for c in counts] == m["gmres"][:STEPS]
+            assert [tuple(c) for c in ranks[r]["counts"]] == counts
+        assert [c[0] for c in counts] == m["newton"][:STEPS]
+        assert [c[1] for c in counts] == m["gmres"][:STEPS]
