@@ -122,7 +122,9 @@ def save_config(cfg, path=None) -> str:
             sections.append((name, [(f.name, getattr(sub, f.name)) for f in dataclasses.fields(sub)
                                     if f.name != "gmres"]))
     g = cfg.solver.gmres
-    sections.append(("gmres", [(f.name, getattr(g, f.name)) for f in dataclasses.fields(g)]))
+    # the extension field is written only when it differs from the reference's behaviour
+    sections.append(("gmres", [(f.name, getattr(g, f.name)) for f in dataclasses.fields(g)
+                               if not (f.name == "orthogonalization" and getattr(g, f.name) == "mgs")]))
     lines = []
     for name, items in sections:
         lines.append(f"[{name}]")
