@@ -4,8 +4,8 @@ arithmetic and colour order, csrc/precond.cu):
   * parity runs (k_sgs_run: one launch per same-parity run of colours, the
     default; k_sgs_runs_coop for the coarsest level),
   * 2D temporally blocked calls (k_sgs_smooth2, UC_SGS_SMOOTH2=1),
-  * the 2D coarsest level resident in shared memory (k_coarse2d; UC_COARSE2D=0
-    selects the tiled cooperative runs).
+  * the coarsest level resident in shared memory (k_coarse2d / k_coarse3d;
+    UC_COARSE2D=0 selects the tiled cooperative runs).
 Both zero-started (SGS kind, pre-smoothing) and non-zero-started
 (post-smoothing inside the V-cycle) calls are covered, on meshes whose sizes
 exercise partial tiles and several chunks."""
@@ -56,9 +56,9 @@ def test_smoothers_bitwise(model, counts, kind, sweeps):
     ref = _apply(uc, mesh, k, st, v, kind, sweeps, {"UC_SGS_PERCOLOR": "1"})
     runs = _apply(uc, mesh, k, st, v, kind, sweeps, {})
     assert np.array_equal(ref.view(np.int64), runs.view(np.int64))
+    # coarsest level by tiled runs instead of the resident k_coarse2d / k_coarse3d
+    tiled = _apply(uc, mesh, k, st, v, kind, sweeps, {"UC_COARSE2D": "0"})
+    assert np.array_equal(ref.view(np.int64), tiled.view(np.int64))
     if dim == 2:
         sm2 = _apply(uc, mesh, k, st, v, kind, sweeps, {"UC_SGS_SMOOTH2": "1"})
         assert np.array_equal(ref.view(np.int64), sm2.view(np.int64))
-        # coarsest level by tiled runs instead of the resident k_coarse2d
-        tiled = _apply(uc, mesh, k, st, v, kind, sweeps, {"UC_COARSE2D": "0"})
-        assert np.array_equal(ref.view(np.int64), tiled.view(np.int64))
