@@ -44,6 +44,8 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# testing only: N > 1 ranks sharing GPUs through the host-staged transport
+HOST_TRANSPORT = os.environ.get("UC_BENCH_HOST_TRANSPORT") == "1"
 
 WORKLOADS = {
     # name: model, dim, extents, counts, theta, dt, step (synthetic states), Newton dt
@@ -284,7 +286,8 @@ def run_slabs(args, w, rank, world, local, dist, emulate=0):
     mesh = uc.build_mesh(w["dim"], extents, counts)
     kern = uc.FreeGrowthKernel() if w["model"] == "free_growth" else uc.AlloyKernel()
     sc = uc.ThetaScheme(w["theta"], w["dt"], w["step"])
-    grp = SlabGroup.local(mesh, kern, nslab) if emulate else SlabGroup.from_torch_dist(mesh, kern)
+    grp = (SlabGroup.local(mesh, kern, nslab) if emulate
+           else SlabGroup.from_torch_dist(mesh, kern, transport="host" if HOST_TRANSPORT else "nccl"))
     nlocs = [(hi - lo) * grp.plane for lo, hi in grp.slabs]
     rng = np.random.default_rng(11 + rank)
 
@@ -432,7 +435,8 @@ def run_slabs(args, w, rank, world, local, dist, emulate=0):
             "config": {"workload": args.workload, "model": w["model"], "dim": w["dim"], "counts": counts,
                        "dof": D_glob, "dof_per_step": 2 * D_glob,
                        "parallelism": (f"slab x{nslab} emulated in one process (testing)" if emulate
-                                       else f"slab x{world} (NCCL ghost planes + allreduce)"),
+                                       else f"slab x{world} host-staged transport, GPUs shared (testing)"
+                                       if HOST_TRANSPORT else f"slab x{world} (NCCL ghost planes + allreduce)"),
                        "l2": "per-rank inputs larger than L2; no flush"},
             "gpu_launches": 5 * args.steps, "clocks": clk.summary(), "roofline": roofline,
             "e2e": e2e, "cpu_baseline": cpu, "newton": newton,
@@ -520,6 +524,8 @@ def main():
 
     import torch
 
+    if HOST_TRANSPORT:
+        local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dist = None
     if args.emulate_slabs > 1 and world == 1:
@@ -528,8 +534,17 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if HOST_TRANSPORT:
+            # testing the N > 1 path on a 1-GPU lease: ranks share the devices,
+            # gloo + the library's host-staged transport instead of NCCL
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         run_slabs(args, w, rank, world, local, dist)
+        if HOST_TRANSPORT:
+            from paper_2006_16764_b200 import _lib as L
+
+            L.load().uc_comm_finalize()
         dist.destroy_process_group()
         return
 

@@ -85,7 +85,7 @@ int uc_ctx_create(const uc_mesh_desc* mesh, const uc_model_params* params, void*
   c->stream = (cudaStream_t)stream;
   cudaError_t e = cudaGetDevice(&c->device);
   if (e == cudaSuccess) e = cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, c->device);
-  if (e == cudaSuccess) e = cudaMalloc(&c->partials, sizeof(double) * UC_RED_GRID_MAX);
+  if (e == cudaSuccess) e = cudaMalloc(&c->partials, sizeof(double) * UC_MDOT_B * UC_RED_GRID_MAX);
   if (e == cudaSuccess) e = cudaMalloc(&c->ticket, sizeof(unsigned int) * 4);
   if (e == cudaSuccess) e = cudaMemset(c->ticket, 0, sizeof(unsigned int) * 4);
   if (e == cudaSuccess) e = cudaMalloc(&c->scal, sizeof(double) * UC_SCAL_SLOTS);

@@ -341,7 +341,6 @@ static int arnoldi_group(const Group& G, const int64_t* n, const double* const* 
 // distributed step needs three global sums (two of k+1 values and the norm)
 // instead of 2(k+1) scalar ones.  Opt-in (GmresConfig.orthogonalization).
 // ---------------------------------------------------------------------------
-#define UC_MDOT_B 8
 struct MdotArgs {
   const double* v[UC_MDOT_B];
   int nb;
@@ -436,7 +435,7 @@ static int cgs2_group(const Group& G, const int64_t* n, const double* const* con
     if (sum && (rc = global_sum_n(G, slot.data(), m, s))) return rc;
     for (int i = 0; i < ns; ++i) {
       uc_ctx* c = G[i];
-      static MupdArgs u;
+      MupdArgs u;
       u.m = m;
       for (int j = 0; j < m; ++j) u.v[j] = basis[i][j];
       k_cgs_update<<<ew_grid(c, n[i]), 256, 0, s>>>(n[i], u, slot[i], w[i], pass == 1 ? c->scal : nullptr);

@@ -33,6 +33,7 @@ struct Precond;  // precond.cu
 // Reduction geometry: fixed so the summation tree depends on n only.
 #define UC_RED_THREADS 256
 #define UC_RED_GRID_MAX 1184
+#define UC_MDOT_B 8  // dots per k_mdot launch (blas.cu); partials hold UC_MDOT_B x UC_RED_GRID_MAX
 #define UC_SCAL_SLOTS 2048
 
 struct uc_ctx {
@@ -43,7 +44,7 @@ struct uc_ctx {
   int device = 0;
   int num_sms = 148;
   // reduction workspace
-  double* partials = nullptr;    // [UC_RED_GRID_MAX]
+  double* partials = nullptr;    // [UC_MDOT_B * UC_RED_GRID_MAX]
   unsigned int* ticket = nullptr;
   double* scal = nullptr;        // [scal_cap] device scalars (grown on demand by the Arnoldi step)
   double* pinned = nullptr;      // [scal_cap] pinned host staging

@@ -71,3 +71,31 @@ def test_cgs2_config_validation():
 
     with pytest.raises(ValueError):
         uc.GmresConfig(orthogonalization="householder")
+
+
+@pytest.mark.parametrize("n", [3_000_000, 8_400_000])
+def test_cgs2_long_vectors(n):
+    """Vectors long enough that the reduction grid is at its cap (k_mdot keeps
+    UC_MDOT_B x grid partials) and k >= 8 (several k_mdot launches per pass):
+    h and the new basis vector agree with a torch fp64 CGS2 and with MGS."""
+    from paper_2006_16764_b200 import device as D
+
+    g = torch.Generator(device="cuda").manual_seed(3)
+    k = 11
+    A = torch.randn(n, k + 1, device="cuda", dtype=torch.float64, generator=g)
+    Q, _ = torch.linalg.qr(A)
+    basis = [Q[:, j].contiguous() for j in range(k + 1)]
+    w0 = torch.randn(n, device="cuda", dtype=torch.float64, generator=g)
+    ref_w = w0.clone()
+    h_ref = torch.zeros(k + 1, device="cuda", dtype=torch.float64)
+    for _ in range(2):
+        hp = torch.stack([b @ ref_w for b in basis])
+        ref_w = ref_w - torch.stack(basis, 1) @ hp
+        h_ref += hp
+    nrm = float(ref_w.norm())
+    for cgs2 in (True, False):
+        h, v, broke = D.arnoldi(lambda x: w0.clone(), basis, k, 1.0, cgs2=cgs2)
+        assert not broke and np.isfinite(h).all()
+        assert np.allclose(h[: k + 1], h_ref.cpu().numpy(), rtol=0, atol=1e-9)
+        assert abs(h[k + 1] - nrm) <= 1e-9 * nrm
+        assert float((v - ref_w / nrm).abs().max()) <= 1e-9
