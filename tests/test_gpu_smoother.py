@@ -1,9 +1,8 @@
 """The three multicolor smoother implementations agree BITWISE (same row
 arithmetic and colour order, csrc/precond.cu):
   * colour-by-colour passes (k_sgs_color, UC_SGS_PERCOLOR=1),
-  * parity runs (k_sgs_run: one launch per same-parity run of colours, the
-    default; k_sgs_runs_coop for the coarsest level),
-  * 2D temporally blocked calls (k_sgs_smooth2, UC_SGS_SMOOTH2=1),
+  * parity runs (k_run2 / k_run3: one launch per same-parity run of colours,
+    the default; k_sgs_runs_coop for the coarsest level),
   * the coarsest level resident in shared memory (k_coarse2d / k_coarse3d;
     UC_COARSE2D=0 selects the tiled cooperative runs).
 Both zero-started (SGS kind, pre-smoothing) and non-zero-started
@@ -39,7 +38,8 @@ def _apply(uc, mesh, k, st, v, kind, sweeps, env):
 
 @pytest.mark.parametrize("model,counts", CASES)
 @pytest.mark.parametrize("kind,sweeps", [("sgs", 2), ("vcycle", 2), ("vcycle", 1)])
-def test_smoothers_bitwise(model, counts, kind, sweeps):
+@pytest.mark.parametrize("state", ["random", "patch"])
+def test_smoothers_bitwise(model, counts, kind, sweeps, state):
     import paper_2006_16764_b200 as uc
 
     dim = len(counts)
@@ -51,6 +51,13 @@ def test_smoothers_bitwise(model, counts, kind, sweeps):
         st = np.concatenate([0.5 + 0.3 * rng.standard_normal(n), 1 + 0.2 * rng.standard_normal(n)])
     else:
         st = np.concatenate([np.tanh(rng.standard_normal(n)), -0.5 + 0.4 * rng.standard_normal(n)])
+    if state == "patch":
+        # constant fields with a perturbed patch: mostly shared (uniform) stencil rows
+        shape = mesh.node_shape[::-1]
+        keep = np.zeros(shape, bool)
+        keep[tuple(slice(s // 3, s // 3 + max(2, s // 5)) for s in shape)] = True
+        keep = keep.ravel()
+        st = np.where(np.concatenate([keep, keep]), st, np.concatenate([np.full(n, st[0]), np.full(n, st[n])]))
     st = torch.tensor(st, device="cuda")
     v = torch.tensor(rng.standard_normal(2 * n), device="cuda")
     ref = _apply(uc, mesh, k, st, v, kind, sweeps, {"UC_SGS_PERCOLOR": "1"})
@@ -59,6 +66,6 @@ def test_smoothers_bitwise(model, counts, kind, sweeps):
     # coarsest level by tiled runs instead of the resident k_coarse2d / k_coarse3d
     tiled = _apply(uc, mesh, k, st, v, kind, sweeps, {"UC_COARSE2D": "0"})
     assert np.array_equal(ref.view(np.int64), tiled.view(np.int64))
-    if dim == 2:
-        sm2 = _apply(uc, mesh, k, st, v, kind, sweeps, {"UC_SGS_SMOOTH2": "1"})
-        assert np.array_equal(ref.view(np.int64), sm2.view(np.int64))
+    # every row on its explicit stencil (no shared-row fast paths)
+    expl = _apply(uc, mesh, k, st, v, kind, sweeps, {"UC_PC_NO_UNIFORM": "1"})
+    assert np.array_equal(ref.view(np.int64), expl.view(np.int64))
