@@ -69,7 +69,9 @@ def test_smoothers_bitwise(model, counts, kind, sweeps, state):
     # every row on its explicit stencil (no shared-row fast paths)
     expl = _apply(uc, mesh, k, st, v, kind, sweeps, {"UC_PC_NO_UNIFORM": "1"})
     assert np.array_equal(ref.view(np.int64), expl.view(np.int64))
-    # 3D V-cycle residuals by the row-gather kernel instead of the marching tiles
-    if kind == "vcycle" and dim == 3:
-        alt = _apply(uc, mesh, k, st, v, kind, sweeps, {"UC_RESID_GATHER": "1"})
-        assert np.array_equal(ref.view(np.int64), alt.view(np.int64))
+    # V-cycle residuals by the row-gather kernel (and in 3D by node lines)
+    # instead of the node lines (2D) / marching tiles (3D)
+    if kind == "vcycle":
+        for env in [{"UC_RESID_GATHER": "1"}] + ([{"UC_RESID_LINE3": "1"}] if dim == 3 else []):
+            alt = _apply(uc, mesh, k, st, v, kind, sweeps, env)
+            assert np.array_equal(ref.view(np.int64), alt.view(np.int64)), env
