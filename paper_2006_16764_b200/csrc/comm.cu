@@ -101,6 +101,19 @@ static int host_flush(std::vector<PendingOp>& ops, cudaStream_t s) {
 
 bool comm_is_host() { return g_host.active; }
 
+void comm_rank_world(int& rank, int& world) {
+  if (g_host.active) {
+    rank = g_host.rank;
+    world = g_host.nranks;
+  } else if (g_nccl.comm) {
+    rank = g_nccl.rank;
+    world = g_nccl.nranks;
+  } else {
+    rank = 0;
+    world = 1;
+  }
+}
+
 static int nccl_load(const char* path) {
   if (g_nccl.handle) return UC_OK;
   void* h = dlopen(path && path[0] ? path : "libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);

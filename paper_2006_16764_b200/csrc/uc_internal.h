@@ -83,6 +83,7 @@ struct PlaneAddr {
 // comm.cu
 bool group_has_remote(const Group& g);
 bool comm_is_host();  // remote neighbours go through the host-staged transport
+void comm_rank_world(int& rank, int& world);  // this process's rank and the number of ranks (0, 1 without a communicator)
 int exchange(const Group& g, const PlaneAddr& addr, bool dir_up, bool dir_down, cudaStream_t s);
 int global_sum(const Group& g, double* const* slots, bool do_sqrt, cudaStream_t s);
 int global_sum_n(const Group& g, double* const* slots, int n, cudaStream_t s);

@@ -6,7 +6,8 @@ so the ranks use the library's host-staged transport (uc_comm_init_host: the
 same call sites, planes staged through pinned host buffers and moved by
 torch.distributed over gloo).  Results must be bitwise those of the same two
 slabs emulated in one process (tests/test_gpu_slabs.py), and the alloy run
-must reproduce the reference's Newton/GMRES counts."""
+must reproduce the reference's Newton/GMRES counts.  The lexicographic V-cycle
+(the ranks sweeping in turn) equals the emulated slabs bitwise as well."""
 
 import os
 import socket
@@ -48,7 +49,9 @@ def _run(grp, uc, models, k, mesh, m, ortho="mgs"):
     jv = res.jv_device(state, f, v, sp.norm(state))
     pc = SlabPrecond(grp, state, sc, uc.PrecondConfig(ordering="multicolor"))
     mv = pc.apply(v)
-    out = {"f": f, "jv": jv, "mv": mv}
+    # the reference's default ordering: the ranks sweep in turn
+    mv_lex = SlabPrecond(grp, state, sc, uc.PrecondConfig(ordering="lexicographic")).apply(v)
+    out = {"f": f, "jv": jv, "mv": mv, "mv_lex": mv_lex}
     prev = sp.clone(state)
     counts = []
     for step in range(STEPS):
