@@ -257,9 +257,7 @@ def vcycle_bytes(pc, N, dim):
         total += 8 * rows[l + 1] + 16 * R  # prolong-add
 
     for c in range(cfg.cycles):
-        cyc(0)
-        if c > 0:
-            total += (stencil[0] + 24) * rows[0] + 24 * rows[0]  # residual + x += e
+        cyc(0)  # later cycles start from x (no defect residual, no x += e)
     return 2 * total  # both field blocks
 
 
