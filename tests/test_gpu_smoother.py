@@ -70,8 +70,10 @@ def test_smoothers_bitwise(model, counts, kind, sweeps, state):
     expl = _apply(uc, mesh, k, st, v, kind, sweeps, {"UC_PC_NO_UNIFORM": "1"})
     assert np.array_equal(ref.view(np.int64), expl.view(np.int64))
     # V-cycle residuals by the row-gather kernel (and in 3D by node lines)
-    # instead of the node lines (2D) / marching tiles (3D)
+    # instead of the node lines (2D) / marching tiles (3D); x gathered back into
+    # one vector between the cycles
     if kind == "vcycle":
-        for env in [{"UC_RESID_GATHER": "1"}] + ([{"UC_RESID_LINE3": "1"}] if dim == 3 else []):
+        for env in [{"UC_RESID_GATHER": "1"}, {"UC_CYCLE_COPYBACK": "1"}] + \
+                   ([{"UC_RESID_LINE3": "1"}] if dim == 3 else []):
             alt = _apply(uc, mesh, k, st, v, kind, sweeps, env)
             assert np.array_equal(ref.view(np.int64), alt.view(np.int64)), env
