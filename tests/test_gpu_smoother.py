@@ -71,9 +71,9 @@ def test_smoothers_bitwise(model, counts, kind, sweeps, state):
     assert np.array_equal(ref.view(np.int64), expl.view(np.int64))
     # V-cycle residuals by the row-gather kernel (and in 3D by node lines)
     # instead of the node lines (2D) / marching tiles (3D); x gathered back into
-    # one vector between the cycles
+    # one vector between the cycles; 2D residual and restriction unfused
     if kind == "vcycle":
-        for env in [{"UC_RESID_GATHER": "1"}, {"UC_CYCLE_COPYBACK": "1"}] + \
+        for env in [{"UC_RESID_GATHER": "1"}, {"UC_CYCLE_COPYBACK": "1"}, {"UC_RESID_RESTRICT": "0"}] + \
                    ([{"UC_RESID_LINE3": "1"}] if dim == 3 else []):
             alt = _apply(uc, mesh, k, st, v, kind, sweeps, env)
             assert np.array_equal(ref.view(np.int64), alt.view(np.int64)), env
