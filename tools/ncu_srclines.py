@@ -31,6 +31,8 @@ for x in r[1:]:
             sass[o.split('.')[0]]+=(int(x[ie]) if x[ie].isdigit() else 0)
 tot=sum(l[2] for l in lines)
 print('total warp inst',tot)
+# opcode shares relative to the per-line total (a SASS row listed under several
+# inlined source lines counts once per line)
 print(', '.join(f"{o}:{n*100/tot:.1f}" for o,n in sass.most_common(24)))
 lines.sort(key=lambda l:-l[2])
 for l in lines[:45]: print(f"{l[2]*100/tot:5.1f}% {l[0]:>5}: {l[1].strip()[:120]}")
